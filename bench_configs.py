@@ -1,0 +1,118 @@
+"""Secondary bench configurations (bench.py --config 3|4|5): BASELINE.json
+configs[2..4].  Same timing rules as bench.py (events on the launch stream,
+barrier + synchronize both sides, max over ranks)."""
+
+from __future__ import annotations
+
+import statistics
+
+import bench
+
+
+def _time_steps(args, world, fn, local):
+    import torch
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        fn()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    bench.barrier_sync(world)
+    with bench.ClockSampler(local) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            fn()
+        t1.record(stream)
+        bench.barrier_sync(world)
+    return bench.max_over_ranks(t0.elapsed_time(t1) * 1e-3, world), clk.summary()
+
+
+def _base_line(args, world, value, elapsed, clk, config, launches):
+    return {"metric": bench.METRIC, "value": value, "unit": "Gnumbers/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u32 Montgomery / u64 skip + f64 map", "data": "synthetic: derived stream params",
+            "config": config, "clocks": clk, "gpu_launches": launches}
+
+
+def run_other(args, world, rank, local):
+    import torch
+    import paper_1811_11629_b200 as R
+    from paper_1811_11629_b200 import _device, _lib, vecgen
+    from paper_1811_11629_b200.shard import shard_range
+    dev = torch.device("cuda", local)
+    peak = bench.probe_imad_peak(dev)
+
+    if args.config == 3:
+        total, mv, blocks = 1 << 16, 64, 1024
+        first, n = shard_range(total, world, rank)
+        t = R.derive_params_table(R.DEFAULT_MASTER_SEED, first, n, dev=dev)
+        m1, m2, s = vecgen._init_lanes(t.inst, n, mv, 0, 1, dev)
+        out = torch.empty((n, blocks * mv), dtype=torch.float64, device=dev)
+
+        def fn():
+            _lib.call("rsa_fill", t.inst.data_ptr(), n, mv, blocks, 9, _lib.RSA_FLAG_FAST,
+                      m1.data_ptr(), m2.data_ptr(), s.data_ptr(), None, out.data_ptr(),
+                      blocks * mv, _device.stream(dev))
+
+        el, clk = _time_steps(args, world, fn, local)
+        numbers = total * mv * blocks
+        line = _base_line(args, world, numbers * args.steps / el / 1e9, el, clk,
+                          {"workload": "config3: 65536 instances (ids 0..65535), e=9, Mv=64, 1024 blocks, "
+                                       "2^16 f64 each, instance-major, sharded by contiguous id range",
+                           "l2": "32 GiB output per step (> L2)"}, args.steps)
+        per = el / args.steps
+        line["roofline"] = {"bound": "imad", "achieved": bench.w_imad(9) * numbers / world / per / 1e12,
+                            "peak": peak["ops_per_s"] / 1e12, "unit": "Tops/s",
+                            "frac": bench.w_imad(9) * numbers / world / per / peak["ops_per_s"],
+                            "traffic": bench.load_traffic("fill_c3")}
+        return line
+
+    if args.config == 4:
+        total, N = 1 << 20, 1 << 16
+        first, n = shard_range(total, world, rank, align=2)
+        t = R.derive_params_table(R.DEFAULT_MASTER_SEED, first, n, dev=dev)
+        fc = R.FusedConsumer(t)
+        box = {}
+
+        def fn():
+            res = fc.run(N)
+            if world > 1:
+                R.all_reduce_pooled(res)
+            box["res"] = res
+
+        el, clk = _time_steps(args, world, fn, local)
+        numbers = total * N
+        line = _base_line(args, world, numbers * args.steps / el / 1e9, el, clk,
+                          {"workload": "config4 fused consumer: 2^20 instances x 2^16 draws, Mv=1, e=9; "
+                                       "per-instance mean/var/lag-1/64-bin hist + pooled pair correlation; "
+                                       "NCCL all-reduce of pooled stats", "l2": "no stream in HBM"},
+                          args.steps * (3 + (2 if world > 1 else 0)))
+        per = el / args.steps
+        line["roofline"] = {"bound": "imad", "achieved": bench.w_imad(9) * numbers / world / per / 1e12,
+                            "peak": peak["ops_per_s"] / 1e12, "unit": "Tops/s",
+                            "frac": bench.w_imad(9) * numbers / world / per / peak["ops_per_s"],
+                            "traffic": bench.load_traffic("fused")}
+        line["pooled_correlation"] = box["res"].pooled_correlation(total // 2)
+        return line
+
+    # config 5: safe-prime scan of [2^31, 2^32) + 2^20 instance tuples
+    from paper_1811_11629_b200 import paramfactory
+    lo_all, hi_all = 1 << 31, 1 << 32
+    span = (hi_all - lo_all) // world
+    lo = lo_all + rank * span
+    hi = hi_all if rank == world - 1 else lo + span
+    first, n = shard_range(1 << 20, world, rank)
+    paramfactory.safe_prime_table(dev)  # the derivation table (built once, untimed)
+
+    def fn():
+        paramfactory.safe_primes_u32(lo, hi, dev)
+        R.derive_params_table(R.DEFAULT_MASTER_SEED, first, n, dev=dev)
+
+    el, clk = _time_steps(args, world, fn, local)
+    cands = (hi_all - lo_all) // 2
+    line = _base_line(args, world, cands * args.steps / el / 1e9, el, clk,
+                      {"workload": "config5 setup: MR(2,7,61) scan of all 2^30 odd candidates in "
+                                   "[2^31,2^32) + 2^20 instance tuples (ids 0..2^20-1)",
+                       "unit_note": "value = odd candidates per second (scan + tuples in the step)"},
+                      args.steps * 5)
+    line["unit"] = "Gcandidates/s"
+    return line

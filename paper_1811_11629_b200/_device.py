@@ -1,0 +1,34 @@
+"""Device plumbing: torch supplies device memory and the current stream; the
+kernels behind the C ABI do the work.  No GPU means no generation (loud error)."""
+
+from __future__ import annotations
+
+import torch
+
+from ._lib import RsaCudaError
+
+
+def device(dev=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RsaCudaError("rsarand_b200 needs a CUDA device (sm_100a); none is available")
+    if dev is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    d = torch.device(dev)
+    if d.type != "cuda":
+        raise RsaCudaError(f"rsarand_b200 computes on CUDA devices only, got {d}")
+    return torch.device("cuda", d.index if d.index is not None else torch.cuda.current_device())
+
+
+def stream(dev: torch.device) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def u64(values, dev: torch.device) -> torch.Tensor:
+    """uint64 device tensor from Python ints (exact for all of [0, 2^64))."""
+    import numpy as np
+    arr = np.asarray(values, dtype=np.uint64)
+    return torch.from_numpy(arr).to(dev)
+
+
+def to_ints(t: torch.Tensor) -> list[int]:
+    return t.cpu().numpy().tolist()

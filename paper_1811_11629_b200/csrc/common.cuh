@@ -1,0 +1,28 @@
+// common.cuh — launch/error plumbing shared by the C-ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "../../include/rsarand_b200.h"
+
+namespace rsa {
+
+void set_last_error(const char* what, cudaError_t err);
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Report the launch status of the kernel just issued (configuration errors and
+// sticky faults from earlier work); never synchronises.
+inline int launch_status(const char* what) {
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) {
+        set_last_error(what, err);
+        return RSA_ECUDA;
+    }
+    return RSA_OK;
+}
+
+inline unsigned grid_for(uint64_t threads, unsigned block) {
+    return (unsigned)((threads + block - 1) / block);
+}
+
+}  // namespace rsa

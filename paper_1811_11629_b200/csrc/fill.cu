@@ -1,0 +1,226 @@
+// fill.cu — K1 bulk fill, lane initialisation and the float map.
+//
+// Replaces vecgen.next_block_raw / next_block / floats_from_raw
+// (vecgen.py:87-112), the block loop of take_raw (vecgen.py:115-139) for whole
+// blocks, and vecgen.init_vector + skipgen.lane_offset_seeds (vecgen.py:44-69,
+// skipgen.py:119-138).
+//
+// Layout: one thread owns LPT adjacent lanes of one instance and walks them
+// through `blocks` draws (a lane is inherently sequential — SURVEY §5); a warp
+// covers 32*LPT consecutive lanes, so each block's stores are contiguous
+// 8*32*LPT-byte runs (128-bit streaming stores when LPT = 2).  State is read
+// once and written once per launch; the stream itself never re-touches HBM.
+#include "common.cuh"
+#include "draw.cuh"
+
+namespace rsa {
+
+template <int LPT>
+RSA_DEV void store_u64(uint64_t* p, const uint64_t (&v)[LPT]) {
+    if constexpr (LPT == 2) __stcs(reinterpret_cast<ulonglong2*>(p), make_ulonglong2(v[0], v[1]));
+    else __stcs(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v[0]);
+}
+
+template <int LPT>
+RSA_DEV void store_f64(double* p, const double (&v)[LPT]) {
+    if constexpr (LPT == 2) __stcs(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
+    else __stcs(p, v[0]);
+}
+
+// Fast path: E = compile-time exponent (0 = runtime e), LPT lanes per thread.
+template <uint32_t E, int LPT, bool RAW, bool F64>
+__global__ void __launch_bounds__(256)
+k_fill_fast(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t total_lanes,
+            uint64_t blocks, uint64_t* __restrict__ m1, uint64_t* __restrict__ m2,
+            uint64_t* __restrict__ s, uint64_t* __restrict__ raw, double* __restrict__ f64,
+            uint64_t inst_stride) {
+    uint64_t lane = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * LPT;
+    if (lane >= total_lanes) return;
+    uint64_t i = lane / mv;
+    uint32_t g = (uint32_t)(lane - i * mv);
+    const FastInst P = load_fast(inst + i);
+    Lane L[LPT];
+#pragma unroll
+    for (int j = 0; j < LPT; ++j) L[j] = lane_in(P, m1[lane + j], m2[lane + j], s[lane + j]);
+    uint64_t off = i * inst_stride + g;
+    for (uint64_t k = 0; k < blocks; ++k, off += mv) {
+        uint64_t c[LPT];
+#pragma unroll
+        for (int j = 0; j < LPT; ++j) c[j] = draw_fast<E>(P, L[j]);
+        if constexpr (RAW) store_u64<LPT>(raw + off, c);
+        if constexpr (F64) {
+            double r[LPT];
+#pragma unroll
+            for (int j = 0; j < LPT; ++j) r[j] = to_unit(c[j], P.n_float, P.n_recip);
+            store_f64<LPT>(f64 + off, r);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < LPT; ++j) {
+        m1[lane + j] = lane_m1(P, L[j]);
+        m2[lane + j] = lane_m2(P, L[j]);
+        s[lane + j] = L[j].s;
+    }
+}
+
+// General path: any odd prime sizes < 2^32, any prime q with a*a <= q, unit /
+// const skips (test_mode instances, rsacore.py:166-181; vecgen.py:61-68).
+__global__ void __launch_bounds__(256)
+k_fill_general(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t total_lanes,
+               uint64_t blocks, uint64_t* __restrict__ m1, uint64_t* __restrict__ m2,
+               uint64_t* __restrict__ s, uint64_t* __restrict__ raw, double* __restrict__ f64,
+               uint64_t inst_stride) {
+    uint64_t lane = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (lane >= total_lanes) return;
+    uint64_t i = lane / mv;
+    uint32_t g = (uint32_t)(lane - i * mv);
+    const GenInst G = load_gen(inst + i);
+    Lane L;
+    L.s = s[lane];
+    L.x1 = mont_redc(m1[lane], G.p1, G.p1_inv);
+    L.x2 = mont_redc(m2[lane], G.p2, G.p2_inv);
+    uint64_t off = i * inst_stride + g;
+    for (uint64_t k = 0; k < blocks; ++k, off += mv) {
+        uint64_t c = draw_general(G, L);
+        if (raw) raw[off] = c;
+        if (f64) f64[off] = to_unit(c, G.n_float, G.n_recip);
+    }
+    m1[lane] = mont_mul(L.x1, G.r2_1, G.p1, G.p1_inv);
+    m2[lane] = mont_mul(L.x2, G.r2_2, G.p2, G.p2_inv);
+    s[lane] = L.s;
+}
+
+__global__ void k_floats_from_raw(const uint64_t* __restrict__ raw, uint64_t count, uint64_t n,
+                                  double* __restrict__ out) {
+    double nf = __ull2double_rn(n);
+    double nr = __drcp_rn(nf);
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count;
+         j += (uint64_t)gridDim.x * blockDim.x)
+        out[j] = to_unit(raw[j], nf, nr);
+}
+
+// (hi*2^64 + lo) mod p for p < 2^32.
+RSA_DEV uint32_t mod128_32(uint64_t lo, uint64_t hi, uint32_t p) {
+    uint64_t r64 = (1ull << 32) % p;               // 2^32 mod p
+    r64 = (r64 * r64) % p;                         // 2^64 mod p
+    uint64_t h = hi % p;
+    return (uint32_t)(((h * r64) % p + lo % p) % p);
+}
+
+__global__ void k_init_lanes(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t total_lanes,
+                             uint64_t m0_lo, uint64_t m0_hi, uint64_t s0,
+                             uint64_t* __restrict__ m1, uint64_t* __restrict__ m2,
+                             uint64_t* __restrict__ s) {
+    uint64_t lane = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (lane >= total_lanes) return;
+    uint64_t i = lane / mv;
+    uint32_t g = (uint32_t)(lane - i * mv);
+    const rsa_instance* ip = inst + i;
+    uint32_t p1 = ip->p1, p2 = ip->p2;
+    uint32_t r1 = mod128_32(m0_lo, m0_hi, p1), r2 = mod128_32(m0_lo, m0_hi, p2);
+    if (ip->skip_mode == RSA_SKIP_LCG) {
+        // lane g: s0 * (a^stride)^g mod q (skipgen.py:124-138)
+        uint64_t q = ip->q, stride = (q - 1) / mv;
+        uint64_t A, sg;
+        if (q == Q63) {
+            A = 1;
+            uint64_t b = ip->a, e = stride;
+            while (e) { if (e & 1) A = mulmod_q63(A, b); e >>= 1; if (e) b = mulmod_q63(b, b); }
+            uint64_t t = 1; b = A; e = g;
+            while (e) { if (e & 1) t = mulmod_q63(t, b); e >>= 1; if (e) b = mulmod_q63(b, b); }
+            sg = mulmod_q63(s0, t);
+        } else {
+            A = powmod64(ip->a, stride, q);
+            sg = mulmod64(s0, powmod64(A, g, q), q);
+        }
+        m1[lane] = r1;
+        m2[lane] = r2;
+        s[lane] = sg;
+    } else {
+        // lane g holds m0 + (g+1-mv)*v, steps by mv*v (vecgen.py:61-68)
+        uint64_t v = ip->skip_mode == RSA_SKIP_UNIT ? 1ull : ip->skip_const;
+        uint64_t n = ip->n;
+        uint64_t back = (uint64_t)(mv - 1 - g);
+        uint32_t b1 = (uint32_t)(((back % p1) * (v % p1)) % p1);
+        uint32_t b2 = (uint32_t)(((back % p2) * (v % p2)) % p2);
+        m1[lane] = r1 >= b1 ? r1 - b1 : r1 + (p1 - b1);
+        m2[lane] = r2 >= b2 ? r2 - b2 : r2 + (p2 - b2);
+        s[lane] = mulmod64(mv % n, v % n, n);
+    }
+}
+
+}  // namespace rsa
+
+using namespace rsa;
+
+template <uint32_t E, int LPT>
+static void launch_fast(unsigned grid, cudaStream_t st, const rsa_instance* inst, uint32_t mv,
+                        uint64_t lanes, uint64_t blocks, uint64_t* m1, uint64_t* m2, uint64_t* s,
+                        uint64_t* raw, double* f64, uint64_t stride) {
+    if (raw && f64)
+        k_fill_fast<E, LPT, true, true><<<grid, 256, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride);
+    else if (raw)
+        k_fill_fast<E, LPT, true, false><<<grid, 256, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride);
+    else if (f64)
+        k_fill_fast<E, LPT, false, true><<<grid, 256, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride);
+    else
+        k_fill_fast<E, LPT, false, false><<<grid, 256, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride);
+}
+
+template <int LPT>
+static void dispatch_e(uint32_t e, unsigned grid, cudaStream_t st, const rsa_instance* inst,
+                       uint32_t mv, uint64_t lanes, uint64_t blocks, uint64_t* m1, uint64_t* m2,
+                       uint64_t* s, uint64_t* raw, double* f64, uint64_t stride) {
+    switch (e) {
+        case 3: launch_fast<3, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride); break;
+        case 5: launch_fast<5, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride); break;
+        case 9: launch_fast<9, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride); break;
+        case 17: launch_fast<17, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride); break;
+        case 65537: launch_fast<65537, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride); break;
+        default: launch_fast<0, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride); break;
+    }
+}
+
+extern "C" int rsa_fill(const rsa_instance* inst, uint32_t n_inst, uint32_t mv, uint64_t blocks,
+                        uint32_t e, uint32_t flags, uint64_t* m1, uint64_t* m2, uint64_t* s,
+                        uint64_t* raw_out, double* f64_out, uint64_t inst_stride, void* stream) {
+    if (!inst || !m1 || !m2 || !s || n_inst == 0 || mv == 0 || e == 0) return RSA_EINVAL;
+    uint64_t lanes = (uint64_t)n_inst * mv;
+    if (n_inst > 1 && (raw_out || f64_out) && inst_stride < blocks * (uint64_t)mv) return RSA_EINVAL;
+    if (blocks == 0) return RSA_OK;
+    cudaStream_t st = as_stream(stream);
+    if (flags & RSA_FLAG_FAST) {
+        // two lanes per thread needs even mv and 16-byte aligned output rows
+        bool pair = (mv % 2 == 0) && (n_inst == 1 || inst_stride % 2 == 0) &&
+                    ((uintptr_t)raw_out % 16 == 0) && ((uintptr_t)f64_out % 16 == 0);
+        if (pair)
+            dispatch_e<2>(e, grid_for(lanes / 2, 256), st, inst, mv, lanes, blocks, m1, m2, s, raw_out, f64_out, inst_stride);
+        else
+            dispatch_e<1>(e, grid_for(lanes, 256), st, inst, mv, lanes, blocks, m1, m2, s, raw_out, f64_out, inst_stride);
+        return launch_status("rsa_fill(fast)");
+    }
+    k_fill_general<<<grid_for(lanes, 256), 256, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw_out,
+                                                        f64_out, inst_stride);
+    return launch_status("rsa_fill(general)");
+}
+
+extern "C" int rsa_floats_from_raw(const uint64_t* raw, uint64_t count, uint64_t n, double* out,
+                                   void* stream) {
+    if ((!raw || !out) && count) return RSA_EINVAL;
+    if (n == 0) return RSA_EINVAL;
+    if (count == 0) return RSA_OK;
+    unsigned grid = grid_for(count, 256);
+    if (grid > 148 * 16) grid = 148 * 16;
+    k_floats_from_raw<<<grid, 256, 0, as_stream(stream)>>>(raw, count, n, out);
+    return launch_status("rsa_floats_from_raw");
+}
+
+extern "C" int rsa_init_lanes(const rsa_instance* inst, uint32_t n_inst, uint32_t mv,
+                              uint64_t m0_lo, uint64_t m0_hi, uint64_t s0,
+                              uint64_t* m1, uint64_t* m2, uint64_t* s, void* stream) {
+    if (!inst || !m1 || !m2 || !s || n_inst == 0 || mv == 0) return RSA_EINVAL;
+    uint64_t lanes = (uint64_t)n_inst * mv;
+    k_init_lanes<<<grid_for(lanes, 128), 128, 0, as_stream(stream)>>>(inst, mv, lanes, m0_lo, m0_hi,
+                                                                       s0, m1, m2, s);
+    return launch_status("rsa_init_lanes");
+}

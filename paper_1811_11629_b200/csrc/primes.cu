@@ -1,0 +1,223 @@
+// primes.cu — K3 safe-prime scan, batched primality predicates, find_pair.
+//
+// Replaces paramfactory.safe_primes_in / _odd_prime_mask (paramfactory.py:85-130,
+// a numpy segmented sieve), numtheory.is_prime64 / is_safe_prime
+// (numtheory.py:81-98, trial division + Miller-Rabin) and paramfactory.find_pair
+// (paramfactory.py:195-219, an outward scan of 11-mod-12 positions).
+//
+// Scan: every safe prime above 7 is 11 mod 12, so the candidate sequence is
+// {5, 7} u {first + 12 j}.  Pass 1 tests 8192 consecutive candidates per CTA
+// (one per thread per iteration), packs the verdicts into warp ballots (one
+// u32 word per 32 candidates) and counts them; pass 2 scans the per-CTA counts;
+// pass 3 re-reads the bitmask and writes the primes in ascending order.  Only
+// 1 bit per candidate touches memory, so the scan is bound by the Miller-Rabin
+// IMAD work, not HBM.
+#include "common.cuh"
+#include "modarith.cuh"
+
+namespace rsa {
+
+constexpr int SCAN_BLOCK = 256;
+constexpr int SCAN_ITERS = 32;
+constexpr uint64_t SCAN_PER_CTA = (uint64_t)SCAN_BLOCK * SCAN_ITERS;  // 8192 candidates
+constexpr int WORDS_PER_CTA = (int)(SCAN_PER_CTA / 32);                  // 256
+
+// n is divisible by odd l  <=>  n * l^-1 mod 2^32 <= floor((2^32-1)/l)
+struct DivTest {
+    uint32_t inv, lim;
+};
+constexpr uint32_t cinv32(uint32_t l) {
+    uint32_t x = l;
+    for (int i = 0; i < 5; ++i) x *= 2u - l * x;
+    return x;
+}
+#define DT(l) DivTest{cinv32(l), 0xFFFFFFFFu / (l)}
+__constant__ DivTest c_div[23] = {DT(5),  DT(7),  DT(11), DT(13), DT(17), DT(19), DT(23), DT(29),
+                                  DT(31), DT(37), DT(41), DT(43), DT(47), DT(53), DT(59), DT(61),
+                                  DT(67), DT(71), DT(73), DT(79), DT(83), DT(89), DT(97)};
+#undef DT
+
+RSA_DEV bool has_small_factor(uint32_t n) {
+#pragma unroll
+    for (int i = 0; i < 23; ++i)
+        if (n * c_div[i].inv <= c_div[i].lim) return true;
+    return false;
+}
+
+RSA_DEV bool mr_2_7_61(uint32_t n) {
+    uint32_t ninv = inv32(n);
+    uint32_t onem = (uint32_t)((1ull << 32) % n);
+    uint32_t r2 = (uint32_t)(((uint64_t)onem * onem) % n);
+    return sprp32(n, 2, ninv, onem, r2) && sprp32(n, 7, ninv, onem, r2) &&
+           sprp32(n, 61, ninv, onem, r2);
+}
+
+// Safe-prime predicate for a scan candidate (5, 7, or p = 11 mod 12).
+RSA_DEV bool candidate_is_safe(uint32_t p) {
+    if (p < 10201u) return is_safe_prime32(p);  // small: exact generic path
+    uint32_t q = (p - 1) >> 1;                   // odd, not divisible by 3
+    if (has_small_factor(p) || has_small_factor(q)) return false;
+    return mr_2_7_61(p) && mr_2_7_61(q);
+}
+
+struct ScanRange {
+    uint64_t first;   // first 11-mod-12 candidate
+    uint64_t total;   // nspec + main candidates
+    uint32_t spec[2];
+    uint32_t nspec;
+};
+
+RSA_DEV uint32_t cand_at(const ScanRange& R, uint64_t j) {
+    return j < R.nspec ? R.spec[j] : (uint32_t)(R.first + 12ull * (j - R.nspec));
+}
+
+__global__ void __launch_bounds__(SCAN_BLOCK)
+k_scan_flags(ScanRange R, uint32_t* __restrict__ words, uint32_t* __restrict__ cta_counts) {
+    __shared__ uint32_t warp_cnt[SCAN_BLOCK / 32];
+    const uint64_t base = (uint64_t)blockIdx.x * SCAN_PER_CTA;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t cnt = 0;
+    for (int it = 0; it < SCAN_ITERS; ++it) {
+        uint64_t j = base + (uint64_t)it * SCAN_BLOCK + threadIdx.x;
+        bool ok = j < R.total && candidate_is_safe(cand_at(R, j));
+        uint32_t bal = __ballot_sync(0xffffffffu, ok);
+        if (lane == 0) {
+            words[j >> 5] = bal;
+            cnt += __popc(bal);
+        }
+    }
+    if (lane == 0) warp_cnt[warp] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < SCAN_BLOCK / 32; ++w) t += warp_cnt[w];
+        cta_counts[blockIdx.x] = t;
+    }
+}
+
+// Exclusive scan of the per-CTA counts (single CTA, chunked, deterministic).
+__global__ void __launch_bounds__(1024)
+k_scan_offsets(const uint32_t* __restrict__ counts, uint64_t n, uint64_t* __restrict__ offsets,
+               uint64_t* __restrict__ total) {
+    __shared__ uint64_t part[1024];
+    const uint64_t per = (n + 1023) / 1024;
+    const uint64_t b = threadIdx.x * per, e = min(n, b + per);
+    uint64_t sum = 0;
+    for (uint64_t i = b; i < e; ++i) sum += counts[i];
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t run = 0;
+        for (int t = 0; t < 1024; ++t) { uint64_t v = part[t]; part[t] = run; run += v; }
+        *total = run;
+    }
+    __syncthreads();
+    uint64_t run = part[threadIdx.x];
+    for (uint64_t i = b; i < e; ++i) { offsets[i] = run; run += counts[i]; }
+}
+
+__global__ void __launch_bounds__(WORDS_PER_CTA)
+k_scan_write(ScanRange R, const uint32_t* __restrict__ words, const uint64_t* __restrict__ offsets,
+             uint32_t* __restrict__ out, uint64_t out_cap) {
+    __shared__ uint32_t warp_tot[WORDS_PER_CTA / 32];
+    const uint64_t w = (uint64_t)blockIdx.x * WORDS_PER_CTA + threadIdx.x;
+    const uint32_t bits = words[w];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t c = __popc(bits), incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    uint32_t before = 0;
+    for (int k = 0; k < warp; ++k) before += warp_tot[k];
+    uint64_t pos = offsets[blockIdx.x] + before + incl - c;
+    uint32_t b = bits;
+    while (b) {
+        int bit = __ffs(b) - 1;
+        b &= b - 1;
+        if (pos < out_cap) out[pos] = cand_at(R, w * 32 + bit);
+        ++pos;
+    }
+}
+
+__global__ void k_is_safe(const uint32_t* __restrict__ n, uint64_t count, uint8_t* __restrict__ is_p,
+                          uint8_t* __restrict__ is_s) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t v = n[j];
+        bool pr = is_prime32(v);
+        if (is_p) is_p[j] = pr;
+        if (is_s) is_s[j] = pr && v > 4 && is_prime32((v - 1) >> 1);
+    }
+}
+
+}  // namespace rsa
+
+using namespace rsa;
+
+static bool make_range(uint64_t lo, uint64_t hi, ScanRange* R) {
+    if (hi > (1ull << 32)) return false;
+    if (lo < 2) lo = 2;
+    R->nspec = 0;
+    if (lo <= 5 && 5 < hi) R->spec[R->nspec++] = 5;
+    if (lo <= 7 && 7 < hi) R->spec[R->nspec++] = 7;
+    uint64_t body = lo > 11 ? lo : 11;
+    uint64_t first = body + (11 + 12 - body % 12) % 12;
+    R->first = first;
+    uint64_t main = hi > first ? (hi - first + 11) / 12 : 0;
+    R->total = R->nspec + main;
+    return true;
+}
+
+static uint64_t scan_ctas(const ScanRange& R) { return (R.total + SCAN_PER_CTA - 1) / SCAN_PER_CTA; }
+
+extern "C" uint64_t rsa_safe_prime_scan_scratch_bytes(uint64_t lo, uint64_t hi) {
+    ScanRange R;
+    if (!make_range(lo, hi, &R)) return 0;
+    uint64_t ctas = scan_ctas(R);
+    if (ctas == 0) ctas = 1;
+    uint64_t words = ctas * WORDS_PER_CTA * 4, counts = ((ctas * 4 + 15) / 16) * 16;
+    return words + counts + ctas * 8;
+}
+
+extern "C" int rsa_safe_prime_scan(uint64_t lo, uint64_t hi, uint32_t* out, uint64_t out_cap,
+                                   uint64_t* count, void* scratch, uint64_t scratch_bytes,
+                                   void* stream) {
+    ScanRange R;
+    if (!count || !make_range(lo, hi, &R)) return RSA_EINVAL;
+    if (scratch_bytes < rsa_safe_prime_scan_scratch_bytes(lo, hi) || !scratch) return RSA_EINVAL;
+    if (out_cap && !out) return RSA_EINVAL;
+    cudaStream_t st = as_stream(stream);
+    uint64_t ctas = scan_ctas(R);
+    if (ctas == 0) {
+        cudaError_t err = cudaMemsetAsync(count, 0, sizeof(uint64_t), st);
+        if (err != cudaSuccess) { set_last_error("rsa_safe_prime_scan", err); return RSA_ECUDA; }
+        return RSA_OK;
+    }
+    char* p = static_cast<char*>(scratch);
+    uint32_t* words = reinterpret_cast<uint32_t*>(p);
+    p += ctas * WORDS_PER_CTA * 4;
+    uint32_t* counts = reinterpret_cast<uint32_t*>(p);
+    p += ((ctas * 4 + 15) / 16) * 16;
+    uint64_t* offsets = reinterpret_cast<uint64_t*>(p);
+    k_scan_flags<<<(unsigned)ctas, SCAN_BLOCK, 0, st>>>(R, words, counts);
+    int rc = launch_status("rsa_safe_prime_scan(flags)");
+    if (rc) return rc;
+    k_scan_offsets<<<1, 1024, 0, st>>>(counts, ctas, offsets, count);
+    if ((rc = launch_status("rsa_safe_prime_scan(offsets)"))) return rc;
+    k_scan_write<<<(unsigned)ctas, WORDS_PER_CTA, 0, st>>>(R, words, offsets, out, out_cap);
+    return launch_status("rsa_safe_prime_scan(write)");
+}
+
+extern "C" int rsa_is_safe_prime32(const uint32_t* n, uint64_t count, uint8_t* is_prime,
+                                   uint8_t* is_safe, void* stream) {
+    if (!n && count) return RSA_EINVAL;
+    if (count == 0) return RSA_OK;
+    unsigned grid = grid_for(count, 256);
+    if (grid > 148 * 32) grid = 148 * 32;
+    k_is_safe<<<grid, 256, 0, as_stream(stream)>>>(n, count, is_prime, is_safe);
+    return launch_status("rsa_is_safe_prime32");
+}

@@ -1,0 +1,210 @@
+"""Lane-vectorised bulk draws — the drop-in for rsarand.vecgen.
+
+Mirrors /root/reference/pkg/src/rsarand/vecgen.py (names, arguments, stream
+order, the `_pending` partial-block buffer and error behaviour), with the lane
+arrays held as uint64 CUDA tensors and every step run by the K1 kernel
+(csrc/fill.cu) through the C ABI.  Results are torch tensors on the state's
+device; `out=` may name a preallocated device tensor, or a (pinned) host tensor,
+in which case blocks are generated in chunks and copied back while the next
+chunk computes.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _device, _lib
+from .rsacore import (SKIP_LCG, GeneratorParams, InvalidSeed, device_instance,
+                      instance_flags, validate_params)
+
+
+def _empty_u64(dev) -> torch.Tensor:
+    return torch.empty(0, dtype=torch.uint64, device=dev)
+
+
+@dataclass
+class VectorState:
+    """Mv lanes of (m1, m2, s) sharing one GeneratorParams (vecgen.py:31-41)."""
+
+    params: GeneratorParams
+    mv: int
+    m1: torch.Tensor
+    m2: torch.Tensor
+    s: torch.Tensor
+    draws: int = 0
+    _pending: torch.Tensor | None = field(default=None)
+
+    def __post_init__(self):
+        if self._pending is None:
+            self._pending = _empty_u64(self.m1.device)
+
+    @property
+    def device(self) -> torch.device:
+        return self.m1.device
+
+
+def _split_m0(m0: int) -> tuple[int, int]:
+    return m0 & 0xFFFFFFFFFFFFFFFF, m0 >> 64
+
+
+def _init_lanes(inst: torch.Tensor, n_inst: int, mv: int, m0: int, s0: int, dev):
+    d = inst.device if dev is None else _device.device(dev)
+    lanes = n_inst * mv
+    m1 = torch.empty(lanes, dtype=torch.uint64, device=d)
+    m2 = torch.empty(lanes, dtype=torch.uint64, device=d)
+    s = torch.empty(lanes, dtype=torch.uint64, device=d)
+    lo, hi = _split_m0(m0)
+    if hi >> 64:
+        raise ValueError("m0 must be below 2^128 here (reduce it mod n first)")
+    _lib.call("rsa_init_lanes", inst.data_ptr(), n_inst, mv, lo, hi, s0,
+              m1.data_ptr(), m2.data_ptr(), s.data_ptr(), _device.stream(d))
+    return m1, m2, s
+
+
+def init_vector(params: GeneratorParams, m0: int = 0, s0: int = 1, mv: int = 1,
+                device=None) -> VectorState:
+    """VectorState seeded like the scalar init, with lane offsets (vecgen.py:44-69)."""
+    validate_params(params)
+    if mv < 1:
+        raise ValueError("lane count must be >= 1")
+    if m0 < 0 or s0 < 0:
+        raise InvalidSeed("seeds must be nonnegative")
+    if params.skip_mode == SKIP_LCG:
+        s0 = s0 % params.skip.q
+        if s0 == 0:
+            raise InvalidSeed(f"s0={s0} is divisible by q")
+    d = _device.device(device)
+    inst = device_instance(params, d)
+    m1, m2, s = _init_lanes(inst, 1, mv, m0 % params.n, s0, d)
+    return VectorState(params=params, mv=mv, m1=m1, m2=m2, s=s)
+
+
+def _fill(state: VectorState, blocks: int, raw: torch.Tensor | None, f64: torch.Tensor | None) -> None:
+    """Advance all lanes `blocks` steps, writing block-major outputs."""
+    if blocks <= 0:
+        return
+    p = state.params
+    d = state.device
+    inst = device_instance(p, d)
+    _lib.call("rsa_fill", inst.data_ptr(), 1, state.mv, blocks, p.e, instance_flags(p),
+              state.m1.data_ptr(), state.m2.data_ptr(), state.s.data_ptr(),
+              raw.data_ptr() if raw is not None else None,
+              f64.data_ptr() if f64 is not None else None,
+              blocks * state.mv, _device.stream(d))
+    state.draws += blocks * state.mv
+
+
+def next_block_raw(state: VectorState) -> torch.Tensor:
+    """Advance every lane one step; the Mv raw ciphertexts (vecgen.py:87-100)."""
+    out = torch.empty(state.mv, dtype=torch.uint64, device=state.device)
+    _fill(state, 1, out, None)
+    return out
+
+
+def floats_from_raw(raw: torch.Tensor, params: GeneratorParams, out: torch.Tensor | None = None) -> torch.Tensor:
+    """r = min(fl(c)/fl(n), 1-2^-53) elementwise (vecgen.py:103-107)."""
+    if raw.device.type != "cuda":
+        raise _lib.RsaCudaError("floats_from_raw expects a CUDA uint64 tensor")
+    raw = raw.contiguous()
+    if out is None:
+        out = torch.empty(raw.shape, dtype=torch.float64, device=raw.device)
+    _lib.call("rsa_floats_from_raw", raw.data_ptr(), raw.numel(), params.n, out.data_ptr(),
+              _device.stream(raw.device))
+    return out
+
+
+def next_block(state: VectorState) -> torch.Tensor:
+    """Advance one step; the Mv doubles in lane order (vecgen.py:110-112)."""
+    out = torch.empty(state.mv, dtype=torch.float64, device=state.device)
+    _fill(state, 1, None, out)
+    return out
+
+
+def _take_device(state: VectorState, count: int, out: torch.Tensor, floats: bool) -> None:
+    """Exactly `count` values in stream order into the device tensor `out`,
+    honouring and refilling the partial-block buffer (vecgen.py:115-139)."""
+    have = 0
+    pend = state._pending
+    if pend.numel():
+        k = min(count, pend.numel())
+        if floats:
+            floats_from_raw(pend[:k], state.params, out[:k])
+        else:
+            out[:k].copy_(pend[:k])
+        state._pending = pend[k:]
+        have = k
+    need = count - have
+    full = need // state.mv
+    if full:
+        seg = out[have:have + full * state.mv]
+        _fill(state, full, None if floats else seg, seg if floats else None)
+        have += full * state.mv
+    tail = count - have
+    if tail:
+        block = next_block_raw(state)
+        if floats:
+            floats_from_raw(block[:tail], state.params, out[have:])
+        else:
+            out[have:].copy_(block[:tail])
+        state._pending = block[tail:]
+
+
+# chunk of whole blocks generated per D2H hop when `out` is on the host
+_HOST_CHUNK_VALUES = 1 << 25
+
+
+def _take(state: VectorState, count: int, out, floats: bool) -> torch.Tensor:
+    if count < 0:
+        raise ValueError("count must be >= 0")
+    dtype = torch.float64 if floats else torch.uint64
+    if out is None:
+        out = torch.empty(count, dtype=dtype, device=state.device)
+    if out.dtype != dtype or out.numel() < count or not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous {dtype} tensor with >= {count} elements")
+    out = out[:count]
+    if out.device.type == "cuda":
+        _take_device(state, count, out, floats)
+        return out
+    _take_to_host(state, count, out, floats)
+    return out
+
+
+def _take_to_host(state: VectorState, count: int, out: torch.Tensor, floats: bool) -> None:
+    """Generate on the device in whole-block chunks and stream them to the host
+    buffer; chunk i+1 computes while chunk i copies (two staging buffers, a
+    copy stream, events)."""
+    d = state.device
+    dtype = out.dtype
+    chunk = max(state.mv, (_HOST_CHUNK_VALUES // state.mv) * state.mv)
+    stage = [torch.empty(min(chunk, count), dtype=dtype, device=d) for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]
+    comp = torch.cuda.current_stream(d)
+    copy = torch.cuda.Stream(d)
+    pos, k = 0, 0
+    while pos < count:
+        n = min(chunk, count - pos)
+        buf = stage[k & 1]
+        if k >= 2:
+            comp.wait_event(done[k & 1])  # staging buffer free again
+        _take_device(state, n, buf[:n], floats)
+        ready = torch.cuda.Event()
+        ready.record(comp)
+        copy.wait_event(ready)
+        with torch.cuda.stream(copy):
+            out[pos:pos + n].copy_(buf[:n], non_blocking=True)
+            done[k & 1].record(copy)
+        pos += n
+        k += 1
+    copy.synchronize()
+
+
+def take_raw(state: VectorState, count: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Exactly count raw values in stream order (vecgen.py:115-139)."""
+    return _take(state, count, out, floats=False)
+
+
+def take_floats(state: VectorState, count: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Exactly count doubles in stream order (vecgen.py:142-144)."""
+    return _take(state, count, out, floats=True)

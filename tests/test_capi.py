@@ -1,0 +1,76 @@
+"""C ABI surface (no GPU needed): the library builds for sm_100a, loads, and
+exports exactly what include/rsarand_b200.h declares, with struct layouts that
+match the Python views."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_1811_11629_b200 import _build, _lib
+
+HEADER = os.path.join(_build.INCLUDE, "rsarand_b200.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    return re.findall(r"^(?:int|uint64_t|const char\*)\s+(rsa_\w+)\(", text, flags=re.M)
+
+
+def test_library_builds_and_loads():
+    path = _build.build()
+    assert os.path.exists(path)
+    lib = _lib.load()
+    assert lib.rsa_abi_version() == 1
+    assert lib.rsa_built_arch() == 100
+
+
+def test_every_declared_symbol_exported_and_typed():
+    names = declared_functions()
+    assert len(names) >= 14
+    lib = ctypes.CDLL(_build.LIB)
+    for n in names:
+        assert hasattr(lib, n), n
+        assert n in _lib.PROTOTYPES, n
+    assert set(_lib.PROTOTYPES) == set(names)
+
+
+def test_cubin_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", _build.LIB], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_struct_layouts_match(tmp_path):
+    fields = list(_lib.INSTANCE_DTYPE.names)
+    cfg_fields = [f for f, _ in _lib.SetupConfig._fields_]
+    src = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void){"]
+    src.append('printf("%zu %zu %zu\\n", sizeof(rsa_instance), sizeof(rsa_setup_config), sizeof(rsa_fused_stat));')
+    for f in fields:
+        src.append(f'printf("%zu\\n", offsetof(rsa_instance, {f}));')
+    for f in cfg_fields:
+        src.append(f'printf("%zu\\n", offsetof(rsa_setup_config, {f}));')
+    src.append("return 0;}")
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(src))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-o", str(exe), str(c)], check=True)
+    vals = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
+    sizes = list(map(int, vals[:3]))
+    offs = list(map(int, vals[3:]))
+    assert sizes == [128, ctypes.sizeof(_lib.SetupConfig), _lib.FUSED_STAT_DTYPE.itemsize]
+    assert offs[:len(fields)] == [_lib.INSTANCE_DTYPE.fields[f][1] for f in fields]
+    assert offs[len(fields):] == [getattr(_lib.SetupConfig, f).offset for f in cfg_fields]
+
+
+def test_argument_errors_need_no_gpu():
+    lib = _lib.load()
+    # invalid arguments are rejected before any launch (status, not a crash)
+    assert lib.rsa_fill(None, 1, 1, 1, 9, 1, None, None, None, None, None, 1, None) == _lib.RSA_EINVAL
+    assert lib.rsa_fused_stats(None, 3, 1, 9, None, None, None, None, None, None) == _lib.RSA_EINVAL
+    assert lib.rsa_safe_prime_scan_scratch_bytes(0, (1 << 32) + 1) == 0
+    assert lib.rsa_safe_prime_scan_scratch_bytes(1 << 31, 1 << 32) > 0

@@ -1,0 +1,258 @@
+"""K1 bulk fill parity on the B200: the CUDA path through the drop-in API /
+C ABI against the reference's golden vectors and the CPU oracles, bit-exact
+(integer ciphertexts and float64 outputs alike)."""
+
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1811_11629_b200 as R
+from paper_1811_11629_b200 import _lib, rsacore, skipgen, vecgen
+from conftest import sha
+from oracle import coracle
+from oracle import rsa_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def u64np(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def p0(golden_regression):
+    g = golden_regression["params"]
+    return rsacore.make_params(g["p1"], g["p2"], g["e"], skipgen.SkipParams.create(g["a"]))
+
+
+def test_regression_vectors_scalar(p0, golden_regression):
+    st = rsacore.init(p0)
+    assert rsacore.take_raws(st, p0, 16) == golden_regression["raw"]
+    assert st.draws == 16
+    assert (st.m1, st.m2, st.s) == tuple(golden_regression["state_after_16"][k] for k in ("m1", "m2", "s"))
+    st = rsacore.init(p0)
+    assert [x.hex() for x in rsacore.take_floats(st, p0, 16)] == golden_regression["f64_hex"]
+    st = rsacore.init(p0)
+    assert [rsacore.next_raw(st, p0) for _ in range(4)] == golden_regression["raw"][:4]
+
+
+def test_scalar_stream_2e16(p0, golden_meta):
+    st = rsacore.init(p0)
+    raw = np.array(rsacore.take_raws(st, p0, 1 << 16), dtype=np.uint64)
+    assert sha(raw.astype("<u8")) == golden_meta["c1_scalar_65536_raw_sha256"]
+
+
+def test_scalar_stream_2e20_vs_c_oracle(p0):
+    """Config 1 at full size: 2^20 sequential draws of one lane."""
+    st = R.init_vector(p0, mv=1)
+    raw = u64np(R.take_raw(st, 1 << 20))
+    one = lambda v: np.array([v], dtype=np.uint64)
+    want, wf = coracle.fill(coracle.params(p0.p1, p0.p2, p0.e, p0.skip.a), one(0), one(0), one(1), 1 << 20)
+    assert np.array_equal(raw, want.reshape(-1))
+    st = R.init_vector(p0, mv=1)
+    assert np.array_equal(u64np(R.take_floats(st, 1 << 20)), wf.reshape(-1))
+
+
+@pytest.mark.parametrize("mv", [1, 2, 8, 64])
+def test_vector_streams(p0, golden_vectors, mv):
+    st = R.init_vector(p0, mv=mv)
+    raw = R.take_raw(st, 4096)
+    assert np.array_equal(u64np(raw), golden_vectors[f"c1_mv{mv}_raw"])
+    st = R.init_vector(p0, mv=mv)
+    assert np.array_equal(u64np(R.take_floats(st, 4096)), golden_vectors[f"c1_mv{mv}_f64"])
+    assert np.array_equal(u64np(R.floats_from_raw(raw, p0)), golden_vectors[f"c1_mv{mv}_f64"])
+
+
+def test_seeded_and_wide(p0, golden_vectors, golden_meta):
+    st = R.init_vector(p0, m0=golden_meta["seeded_m0"], mv=64)
+    assert np.array_equal(u64np(R.take_raw(st, 4096)), golden_vectors["c1_seeded_mv64_raw"])
+    st = R.init_vector(p0, mv=65536)
+    raw = u64np(R.take_raw(st, 2 * 65536))
+    assert sha(raw.astype("<u8")) == golden_meta["c1_mv65536"]["raw_sha256"]
+    st = R.init_vector(p0, mv=65536)
+    f = u64np(R.take_floats(st, 2 * 65536))
+    assert sha(f.astype("<f8")) == golden_meta["c1_mv65536"]["f64_sha256"]
+
+
+def test_partial_takes_and_pending(p0, golden_vectors, golden_meta):
+    st = R.init_vector(p0, mv=8)
+    got = np.concatenate([u64np(R.take_raw(st, k)) for k in golden_meta["take_parts_sizes"]])
+    assert np.array_equal(got, golden_vectors["take_parts_mv8"])
+    # floats drain the same raw pending buffer (vecgen.py:142-144)
+    a, b = R.init_vector(p0, mv=8), R.init_vector(p0, mv=8)
+    parts = [u64np(R.take_floats(a, k)) for k in (3, 13, 0, 5)]
+    assert np.array_equal(np.concatenate(parts), u64np(R.take_floats(b, 21)))
+    assert a.draws == b.draws == 24
+    assert len(R.take_raw(R.init_vector(p0, mv=4), 0)) == 0
+    with pytest.raises(ValueError):
+        R.take_raw(a, -1)
+
+
+def test_chained_calls_equal_one_call(p0):
+    a, b = R.init_vector(p0, mv=256), R.init_vector(p0, mv=256)
+    one = u64np(R.take_raw(a, 256 * 40))
+    parts = np.concatenate([u64np(R.next_block_raw(b)) for _ in range(8)] +
+                           [u64np(R.take_raw(b, 256 * 32))])
+    assert np.array_equal(one, parts)
+    for name in ("m1", "m2", "s"):
+        assert torch.equal(getattr(a, name), getattr(b, name))
+
+
+def test_next_block_matches_floats_of_raw(p0):
+    a, b = R.init_vector(p0, mv=96), R.init_vector(p0, mv=96)
+    for _ in range(5):
+        f = R.next_block(a)
+        r = R.next_block_raw(b)
+        assert torch.equal(f, R.floats_from_raw(r, p0))
+
+
+def _lane_subset_check(p0, golden_vectors, golden_meta, e, blocks=16):
+    pe = dataclasses.replace(p0, e=e)  # e=65537 bypasses validation like the reference recipe
+    mv = golden_meta["c2"]["mv"]
+    d = torch.device("cuda")
+    inst = rsacore.device_instance(pe, d)
+    m1, m2, s = vecgen._init_lanes(inst, 1, mv, golden_meta["seeded_m0"] % pe.n, 1, d)
+    st = vecgen.VectorState(params=pe, mv=mv, m1=m1, m2=m2, s=s)
+    raw = torch.empty(blocks * mv, dtype=torch.uint64, device=d)
+    f64 = torch.empty(blocks * mv, dtype=torch.float64, device=d)
+    vecgen._fill(st, blocks, raw, f64)
+    lanes = golden_vectors["c2_lanes"]
+    raw = u64np(raw).reshape(blocks, mv)[:, lanes]
+    f64 = u64np(f64).reshape(blocks, mv)[:, lanes]
+    assert np.array_equal(raw, golden_vectors[f"c2_e{e}_raw"][:blocks])
+    assert np.array_equal(f64, golden_vectors[f"c2_e{e}_f64"][:blocks])
+
+
+@pytest.mark.parametrize("e", [3, 5, 9, 17, 257, 65537])
+def test_config2_exponents_lane_subset(p0, golden_vectors, golden_meta, e):
+    """Config 2 (Mv = 2^22, seeded m0) for every exponent, against the
+    reference's own lane-subset draws."""
+    _lane_subset_check(p0, golden_vectors, golden_meta, e)
+
+
+def test_config2_full_fill_properties(p0, golden_meta):
+    """2^30 doubles at Mv=2^22 (256 blocks): random lanes bit-exact against
+    the C oracle over all blocks; size-independent properties on the whole."""
+    mv, blocks = 1 << 22, 256
+    st = R.init_vector(p0, m0=golden_meta["seeded_m0"], mv=mv)
+    s_init = u64np(st.s)
+    out = R.take_floats(st, mv * blocks)
+    assert float(out.min()) >= 0.0 and float(out.max()) < 1.0
+    assert abs(float(out.mean()) - 0.5) < 1e-4
+    rng = np.random.default_rng(7)
+    lanes = np.unique(rng.integers(0, mv, size=1024))
+    m0 = golden_meta["seeded_m0"]
+    cp = coracle.params(p0.p1, p0.p2, p0.e, p0.skip.a)
+    m1 = np.full(len(lanes), m0 % p0.p1, dtype=np.uint64)
+    m2 = np.full(len(lanes), m0 % p0.p2, dtype=np.uint64)
+    s = np.ascontiguousarray(s_init[lanes])
+    _, want = coracle.fill(cp, m1, m2, s, blocks, raw=False)
+    got = out.view(blocks, mv)[:, torch.from_numpy(lanes).cuda()].cpu().numpy()
+    assert np.array_equal(got, want)
+    assert np.array_equal(u64np(st.s)[lanes], s)
+
+
+def test_e65537_full_vector(p0, golden_vectors, golden_meta):
+    pe = dataclasses.replace(p0, e=65537)
+    d = torch.device("cuda")
+    inst = rsacore.device_instance(pe, d)
+    m1, m2, s = vecgen._init_lanes(inst, 1, 256, golden_meta["seeded_m0"] % pe.n, 1, d)
+    st = vecgen.VectorState(params=pe, mv=256, m1=m1, m2=m2, s=s)
+    got = np.stack([u64np(R.next_block_raw(st)) for _ in range(8)])
+    assert np.array_equal(got, golden_vectors["c2_e65537_mv256_raw"])
+
+
+def test_miniature_test_mode(golden_vectors, golden_meta):
+    g = golden_meta["miniature"]
+    mini = rsacore.make_params(g["p1"], g["p2"], g["e"],
+                               skipgen.SkipParams.create(g["a"], q=g["q"], allow_weak=True),
+                               test_mode=True)
+    st = rsacore.init(mini)
+    raws = rsacore.take_raws(st, mini, 3036 * 2)
+    assert raws == golden_vectors["mini_scalar_raw"].tolist()
+    assert (st.m1, st.m2, st.s) == (0, 0, 1)  # full period recurs (test_acceptance.py:45-61)
+    v = R.init_vector(mini, mv=3)
+    assert np.array_equal(u64np(R.take_raw(v, 3036 * 3)), golden_vectors["mini_mv3_raw"])
+    assert u64np(R.init_vector(mini, mv=4).s).tolist() == [1, 8, 12, 5]
+
+
+def test_counter_modes(p0, golden_vectors, golden_meta):
+    g = golden_meta["tiny"]
+    tiny = rsacore.make_params(g["p1"], g["p2"], g["e"],
+                               skipgen.SkipParams.create(g["a"], q=g["q"], allow_weak=True),
+                               skip_mode="unit", test_mode=True)
+    st = rsacore.init(tiny)
+    assert rsacore.take_raws(st, tiny, 200) == golden_vectors["tiny_unit_raw"].tolist()
+    assert golden_vectors["tiny_unit_raw"][37] == 48  # the worked Garner example
+    unit9 = rsacore.make_params(p0.p1, p0.p2, 9, p0.skip, skip_mode="unit")
+    for mv in (1, 3, 8):
+        v = R.init_vector(unit9, m0=5, mv=mv)
+        assert np.array_equal(u64np(R.take_raw(v, 64)), golden_vectors[f"unit_m05_mv{mv}_raw"])
+    const9 = rsacore.make_params(p0.p1, p0.p2, 9, p0.skip, skip_mode="const",
+                                 skip_const=golden_meta["const_skip"])
+    v = R.init_vector(const9, mv=7)
+    assert np.array_equal(u64np(R.take_raw(v, 50)), golden_vectors["const_mv7_raw"])
+    st = rsacore.init(const9)
+    assert rsacore.take_raws(st, const9, 50) == golden_vectors["const_mv7_raw"].tolist()
+
+
+def test_clamp_and_float_map(p0, golden_vectors):
+    raw = torch.from_numpy(golden_vectors["clamp_raw"]).cuda()
+    f = u64np(R.floats_from_raw(raw, p0))
+    assert np.array_equal(f, golden_vectors["clamp_f64"])
+    assert f[1] == rsacore.MAX_BELOW_ONE
+    # reciprocal + two Markstein steps == IEEE fl(c)/fl(n), on random and edge ciphertexts
+    rng = np.random.default_rng(11)
+    for n in (p0.n, (1 << 63) - 25 - 4_600_000_000_000 | 1, (1 << 63) + 4_200_000_000_001, 77, 253):
+        c = rng.integers(0, n, size=1 << 22, dtype=np.uint64)
+        c[:8] = [0, 1, n - 1, n - 2, n // 2, n // 3, 1 << 52, (1 << 53) + 1]
+        edges = np.array([1 << k for k in range(64) if (1 << k) < n], dtype=np.uint64)
+        c = np.concatenate([c, edges, edges - np.uint64(1)])
+        want = np.minimum(c.astype(np.float64) / float(n), rsacore.MAX_BELOW_ONE)
+        got = np.empty_like(want)
+        ct = torch.from_numpy(c).cuda()
+        out = torch.empty(len(c), dtype=torch.float64, device="cuda")
+        _lib.call("rsa_floats_from_raw", ct.data_ptr(), len(c), n, out.data_ptr(),
+                  torch.cuda.current_stream().cuda_stream)
+        got = u64np(out)
+        assert np.array_equal(got, want), n
+
+
+def test_lane_seeds(p0, golden_vectors):
+    assert np.array_equal(u64np(skipgen.lane_offset_seeds(p0.skip, 1, 64)), golden_vectors["lane_seeds_mv64"])
+    assert np.array_equal(u64np(skipgen.lane_offset_seeds(p0.skip, 777, 64)),
+                          golden_vectors["lane_seeds_mv64_s0_777"])
+    v = R.init_vector(p0, mv=64)
+    assert np.array_equal(u64np(v.s), golden_vectors["lane_seeds_mv64"])
+
+
+def test_lane_partition_matches_whole(p0):
+    """Halves of the lane vector advanced separately equal the fused update
+    (test_vecgen.py:156-171) — what licenses sharding lanes across GPUs."""
+    whole = R.init_vector(p0, mv=8)
+    halves = []
+    for sl in (slice(0, 4), slice(4, 8)):
+        h = R.init_vector(p0, mv=8)
+        h.m1, h.m2, h.s, h.mv = h.m1[sl].clone(), h.m2[sl].clone(), h.s[sl].clone(), 4
+        halves.append(h)
+    for _ in range(50):
+        blk = u64np(R.next_block(whole))
+        assert np.array_equal(blk, np.concatenate([u64np(R.next_block(h)) for h in halves]))
+
+
+def test_lane_states_distinct(p0):
+    v = R.init_vector(p0, mv=64)
+    R.take_raw(v, 64 * 10_000)
+    assert len(np.unique(u64np(v.s))) == 64
+
+
+def test_take_into_host_buffer(p0):
+    a, b = R.init_vector(p0, mv=1 << 12), R.init_vector(p0, mv=1 << 12)
+    n = (1 << 26) + 12345
+    host = torch.empty(n, dtype=torch.float64).pin_memory()
+    R.take_floats(a, n, out=host)
+    dev = R.take_floats(b, n)
+    assert torch.equal(host, dev.cpu())
+    assert torch.equal(a._pending, b._pending) and a.draws == b.draws

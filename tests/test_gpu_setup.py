@@ -1,0 +1,133 @@
+"""K3 safe-prime scan and K4 instance setup on the B200 against the
+reference's census / derivation fixtures and the C oracle (config 5)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1811_11629_b200 as R
+from paper_1811_11629_b200 import _lib, paramfactory, rsacore, skipgen
+from conftest import sha
+from oracle import coracle
+from oracle import rsa_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def test_full_census(golden_census):
+    sp = paramfactory.safe_primes_u32(1 << 31, 1 << 32).cpu().numpy().view(np.uint32)
+    assert len(sp) == golden_census["safe_primes"] == 3_060_794
+    assert sha(sp.astype("<u4")) == golden_census["sha256_u32le"]
+    tab = paramfactory.safe_prime_table()
+    assert tab.n_sp == 3_060_794 and tab.n_p1 == golden_census["p1_window_count"]
+
+
+@pytest.mark.parametrize("lo,hi", [(2, 5000), (0, 12), (5, 8), (11, 12), ((1 << 31) + 1, (1 << 31) + 100_001),
+                                   ((1 << 32) - 1_000_000, 1 << 32), (3037000000, 3037100000),
+                                   (1_000_000, 1_200_000)])
+def test_scan_windows(lo, hi):
+    got = R.safe_primes_in(lo, hi).cpu().numpy().tolist()
+    want = [p for p in range(max(lo, 2), min(hi, 12)) if O.is_safe_prime(p)]
+    if hi > 11:
+        sp, _ = coracle.census(max(lo, 11), hi)
+        want += sp.tolist()
+    assert got == want
+
+
+def test_segment_stitching():
+    a = R.safe_primes_in(2_000_000, 2_500_000).cpu().numpy()
+    b = R.safe_primes_in(2_500_000, 3_000_000).cpu().numpy()
+    assert np.concatenate([a, b]).tolist() == R.safe_primes_in(2_000_000, 3_000_000).cpu().numpy().tolist()
+
+
+def test_nth_safe_prime():
+    assert R.nth_safe_prime_in(11, 100, 0) == 11
+    assert R.nth_safe_prime_in(11, 100, 1) == 23
+    assert R.nth_safe_prime_in(5, 100, 1) == 7
+    with pytest.raises(R.NotFound):
+        R.nth_safe_prime_in(11, 100, 8)
+    with pytest.raises(ValueError):
+        R.nth_safe_prime_in(100, 100, 0)
+
+
+def test_batched_predicates():
+    rng = np.random.default_rng(3)
+    n = np.concatenate([np.arange(0, 20000, dtype=np.uint32),
+                        rng.integers(1 << 31, 1 << 32, size=200_000, dtype=np.uint64).astype(np.uint32),
+                        np.array([2147483783, 3037000943, 4294967087, 4294967291], dtype=np.uint32)])
+    t = torch.from_numpy(n.view(np.int32)).cuda()
+    isp = torch.empty(len(n), dtype=torch.uint8, device="cuda")
+    iss = torch.empty(len(n), dtype=torch.uint8, device="cuda")
+    _lib.call("rsa_is_safe_prime32", t.data_ptr(), len(n), isp.data_ptr(), iss.data_ptr(),
+              torch.cuda.current_stream().cuda_stream)
+    isp, iss = isp.cpu().numpy().astype(bool), iss.cpu().numpy().astype(bool)
+    sample = list(range(0, len(n), 7))
+    assert [bool(isp[i]) for i in sample] == [O.is_prime(int(n[i])) for i in sample]
+    assert [bool(iss[i]) for i in sample] == [O.is_safe_prime(int(n[i])) for i in sample]
+    assert iss[-4:].tolist() == [True, True, True, False]
+
+
+def test_find_pair(golden_streams):
+    assert list(R.find_pair(3037000943)) == golden_streams["find_pair_anchor"]
+    assert list(R.find_pair(2147483783)) == golden_streams["find_pair_first"]
+    with pytest.raises(R.NotFound):
+        R.find_pair(2147483783, tol=0.0)
+    with pytest.raises(ValueError):
+        R.find_pair((1 << 31) + 1)
+
+
+def test_derive_stream_params_matches_reference(golden_streams):
+    seed = golden_streams["master_seed"]
+    for sid in [0, 1, 2, 3, 7, 100, 511, 61644, 63194, 65535, (1 << 20) - 1]:
+        p = R.derive_stream_params(R.StreamKey(seed, sid))
+        g = golden_streams["streams"][str(sid)]
+        assert (p.p1, p.p2, p.n, p.e, p.skip.a, p.p2inv, p.b) == \
+            (g["p1"], g["p2"], g["n"], g["e"], g["a"], g["p2inv"], g["b"]), sid
+    ex = golden_streams["extra"]
+    p = R.derive_stream_params(R.StreamKey(7, 8), e=17)
+    assert (p.p1, p.p2, p.e) == (ex["e17_id7_seed7"]["p1"], ex["e17_id7_seed7"]["p2"], 17)
+    p = R.derive_stream_params(R.StreamKey(0xBEEF, 3))
+    assert (p.p1, p.p2, p.skip.a) == (ex["seed_beef_id3"]["p1"], ex["seed_beef_id3"]["p2"], ex["seed_beef_id3"]["a"])
+    p = R.derive_stream_params(R.StreamKey(1, 2), multiplier=skipgen.MULTIPLIER_TABLE[5])
+    assert (p.p1, p.p2, p.skip.a) == (ex["mult5_seed1_id2"]["p1"], ex["mult5_seed1_id2"]["p2"],
+                                      skipgen.MULTIPLIER_TABLE[5])
+    p = R.derive_stream_params(R.StreamKey((1 << 64) - 3, 5))
+    assert (p.p1, p.p2) == (ex["seed_big_id5"]["p1"], ex["seed_big_id5"]["p2"])
+    with pytest.raises(ValueError):
+        R.derive_stream_params(R.StreamKey(1, 2), multiplier_table=())
+    with pytest.raises(R.DerivationExhausted):
+        R.derive_stream_params(R.StreamKey(1, 2), e=4)
+
+
+def test_derive_all_2e20(golden_derive_all, golden_streams):
+    """Config 5: 2^20 instance tuples built on the device, packed like the
+    golden digest (computed by the reference), plus device-only constants
+    checked by identity."""
+    n = golden_derive_all["ids"]
+    t = R.derive_params_table(golden_streams["master_seed"], 0, n)
+    rec = t.records()
+    rows = np.zeros(n, dtype=coracle.TUPLE_DTYPE)
+    for f in ("p1", "p2", "a", "p2inv", "n", "b"):
+        rows[f] = rec[f]
+    assert sha(rows[:65536]) == golden_derive_all["sha256_first_65536"]
+    assert sha(rows) == golden_derive_all["sha256"]
+    steps = t.steps.cpu().numpy()
+    assert {str(i): int(steps[i]) for i in np.nonzero(steps)[0]} == golden_derive_all["advanced_ids"]
+    R32 = np.uint64(1 << 32)
+    p1 = rec["p1"].astype(np.uint64)
+    assert ((p1 * rec["p1_inv"].astype(np.uint64)) % R32 == 1).all()
+    assert (rec["n_float"] == rec["n"].astype(np.float64)).all()
+    assert (rec["n_recip"] == 1.0 / rec["n_float"]).all()
+    assert (rec["flags"] == _lib.RSA_FLAG_FAST).all()
+    # a sample against the host packer
+    for j in (0, 1, 61644, 1000, n - 1):
+        host = rsacore._instance_record(t.params(j))[0]
+        for f in ("k1", "k2", "r2_1", "r2_2", "garner", "q1", "q2", "p2_inv"):
+            assert host[f] == rec[j][f], (j, f)
+
+
+def test_table_e_and_errors(golden_streams):
+    t = R.derive_params_table(golden_streams["master_seed"], 0, 64, e=17)
+    assert (t.records()["e"] == 17).all()
+    with pytest.raises(R.DerivationExhausted):
+        R.derive_params_table(0, 0, 4, e=259)
