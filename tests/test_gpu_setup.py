@@ -27,7 +27,7 @@ def test_full_census(golden_census):
                                    (1_000_000, 1_200_000)])
 def test_scan_windows(lo, hi):
     got = R.safe_primes_in(lo, hi).cpu().numpy().tolist()
-    want = [p for p in range(max(lo, 2), min(hi, 12)) if O.is_safe_prime(p)]
+    want = [p for p in range(max(lo, 2), min(hi, 11)) if O.is_safe_prime(p)]
     if hi > 11:
         sp, _ = coracle.census(max(lo, 11), hi)
         want += sp.tolist()

@@ -1,0 +1,90 @@
+"""N>1 host logic on CPU: two gloo ranks each own a contiguous, pair-aligned
+shard of instances (shard.shard_range), reduce their pooled fused statistics
+with fused.all_reduce_pooled, and must agree with the single-process result.
+Per-rank statistics come from the CPU oracle (no GPU here); the collective and
+the pooled-correlation formula are the product code."""
+
+import json
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as tmp
+
+from paper_1811_11629_b200.fused import FusedStats, all_reduce_pooled
+from paper_1811_11629_b200.shard import shard_range
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+N_INST, N = 8, 4096
+
+
+def _draws(ids):
+    from oracle import coracle
+    from oracle import rsa_oracle as O
+    with open(os.path.join(ROOT, "tests", "golden", "streams.json")) as fh:
+        streams = json.load(fh)["streams"]
+    out = np.empty((len(ids), N))
+    one = lambda v: np.array([v], dtype=np.uint64)
+    for j, sid in enumerate(ids):
+        P = O.from_fields(streams[str(sid)])
+        _, f = coracle.fill(coracle.params(P.p1, P.p2, P.e, P.a), one(0), one(0), one(1), N, raw=False)
+        out[j] = f.reshape(-1)
+    return out
+
+
+def _local_stats(first, count) -> FusedStats:
+    """The kernel's per-instance outputs and pooled layout, from oracle draws."""
+    r = _draws(list(range(first, first + count)))
+    s1, s2 = r.sum(1), (r * r).sum(1)
+    lag = (r[:, :-1] * r[:, 1:]).sum(1)
+    xy = np.zeros(count)
+    xy[0::2] = (r[0::2] * r[1::2]).sum(1)
+    stats = np.stack([s1, s2, lag, r[:, 0], r[:, -1], xy], axis=1)
+    hist = np.stack([np.bincount(np.floor(x * 64).astype(int), minlength=64) for x in r])
+    ev = np.arange(count) % 2 == 0  # first is even, so local parity = global parity
+    pooled = np.array([s1.sum(), s2.sum(), xy[ev].sum(), s1[ev].sum(), s1[~ev].sum(),
+                       s2[ev].sum(), s2[~ev].sum()])
+    return FusedStats(N, torch.from_numpy(stats), torch.from_numpy(hist.astype(np.int32)),
+                      torch.from_numpy(pooled), torch.from_numpy(hist.sum(0).astype(np.int64)))
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    first, count = shard_range(N_INST, world, rank, align=2)
+    res = all_reduce_pooled(_local_stats(first, count))
+    q.put((rank, res.pooled_correlation(N_INST // 2), res.pooled_hist.numpy().tolist(),
+           res.pooled.numpy().tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_two_rank_pooled_reduction_matches_single():
+    world = 2
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    whole = _local_stats(0, N_INST)
+    from oracle import rsa_oracle as O
+    ref = O.fused_reference(_draws(list(range(N_INST))))
+    for rank, corr, hist, pooled in got:
+        assert hist == whole.pooled_hist.numpy().tolist() == ref["pooled_hist"].tolist()
+        np.testing.assert_allclose(pooled, whole.pooled.numpy(), rtol=1e-13)
+        assert abs(corr - ref["corr"]) < 1e-11
+        assert abs(corr - whole.pooled_correlation()) < 1e-13
