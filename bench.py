@@ -258,7 +258,10 @@ def run_config2(args, world, rank, local):
         for e in EXPONENTS:
             if events is not None:
                 events[e][0].record(stream)
-            R.take_floats(states[e], count, out=out)
+            if args.one_lane:
+                _fill_flags(states[e], count, out, 8)
+            else:
+                R.take_floats(states[e], count, out=out)
             if events is not None:
                 events[e][1].record(stream)
 
@@ -287,7 +290,8 @@ def run_config2(args, world, rank, local):
     pk = peaks()
     hbm_peak = pk.get("hbm_gbs")
     traffic = load_traffic(f"fill_e{dom}")
-    roofline = {"bound": "imad", "kernel": f"k_fill_fast<{dom},2,false,true> (e={dom})",
+    lpt = 1 if args.one_lane else 2
+    roofline = {"bound": "imad", "kernel": f"k_fill_fast<{dom},{lpt},false,true> (e={dom})",
                 "achieved": imad_ach / 1e12, "peak": peak["ops_per_s"] / 1e12, "unit": "Tops/s",
                 "frac": imad_ach / peak["ops_per_s"], "traffic": traffic,
                 "algorithmic_ops_per_draw": w_imad(dom), "draws_per_launch": count,
@@ -342,6 +346,16 @@ def run_config2(args, world, rank, local):
     return line
 
 
+def _fill_flags(state, count, out, extra):
+    """A/B only: rsa_fill with extra RSA_FLAG_* hints for whole blocks."""
+    from paper_1811_11629_b200 import _device, _lib, rsacore
+    p = state.params
+    inst = rsacore.device_instance(p, state.device)
+    _lib.call("rsa_fill", inst.data_ptr(), 1, state.mv, count // state.mv, p.e,
+              _lib.RSA_FLAG_FAST | extra, state.m1.data_ptr(), state.m2.data_ptr(),
+              state.s.data_ptr(), None, out.data_ptr(), count, _device.stream(state.device))
+
+
 def load_traffic(key: str):
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
@@ -377,6 +391,7 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--one-lane", action="store_true", help="A/B: one lane per thread (RSA_FLAG_ONE_LANE)")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps violates the timing rules", file=sys.stderr)

@@ -47,6 +47,8 @@ extern "C" {
 /* rsa_instance.flags */
 #define RSA_FLAG_FAST 1u   /* q = 2^63-25, p1,p2 in (2^31,2^32), lcg mode: fast kernels */
 #define RSA_FLAG_FIXED 2u  /* unit / const skip: per-lane skip register is constant     */
+#define RSA_FLAG_GENERAL_PATH 4u /* rsa_fill hint: force the general kernel (cross-checks) */
+#define RSA_FLAG_ONE_LANE 8u     /* rsa_fill hint: one lane per thread (tuning / A-B)       */
 
 /*
  * Per-instance constants, 128 bytes, one per generator instance.  The first
@@ -70,7 +72,8 @@ typedef struct rsa_instance {
     double n_float;           /*  88  float(n) (rsacore.py:104)                  */
     double n_recip;           /*  96  RN(1/n_float)                              */
     uint64_t skip_const;      /* 104  const-mode skip value (rsacore.py:91)      */
-    uint64_t reserved2[2];    /* 112                                             */
+    double n_recip_lo;        /* 112  RN((1 - n_float*n_recip) * n_recip): 1/fl(n) ~ hi + lo */
+    uint64_t reserved2;       /* 120                                             */
 } rsa_instance;
 
 /* ---------------------------------------------------------------------------
@@ -90,6 +93,8 @@ typedef struct rsa_instance {
  * RSA_FLAG_FAST an exponent-specialised kernel runs (e in {3,5,9,17,65537}
  * fully unrolled, any other e through the runtime chain); otherwise the
  * general kernel (test-mode sizes, any prime q, unit/const skips) runs.
+ * RSA_FLAG_GENERAL_PATH forces the general kernel (independent cross-check);
+ * RSA_FLAG_ONE_LANE forces one lane per thread.
  * --------------------------------------------------------------------------- */
 int rsa_fill(const rsa_instance* inst, uint32_t n_inst, uint32_t mv, uint64_t blocks,
              uint32_t e, uint32_t flags, uint64_t* m1, uint64_t* m2, uint64_t* s,

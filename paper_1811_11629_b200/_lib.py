@@ -28,16 +28,16 @@ RSA_ECAPACITY = -4
 RSA_EALIGN = -5
 
 RSA_SKIP_LCG, RSA_SKIP_UNIT, RSA_SKIP_CONST = 0, 1, 2
-RSA_FLAG_FAST, RSA_FLAG_FIXED = 1, 2
+RSA_FLAG_FAST, RSA_FLAG_FIXED, RSA_FLAG_GENERAL_PATH, RSA_FLAG_ONE_LANE = 1, 2, 4, 8
 
 # rsa_instance (128 bytes) — field order and offsets mirror the C struct.
 INSTANCE_DTYPE = np.dtype({
     "names": ["p1", "p2", "p1_inv", "p2_inv", "a", "e", "k1", "k2", "r2_1", "r2_2",
               "garner", "p2inv", "q1", "q2", "flags", "skip_mode", "n", "q", "b",
-              "n_float", "n_recip", "skip_const", "reserved2"],
-    "formats": ["<u4"] * 16 + ["<u8"] * 3 + ["<f8", "<f8", "<u8", ("<u8", 2)],
+              "n_float", "n_recip", "skip_const", "n_recip_lo", "reserved2"],
+    "formats": ["<u4"] * 16 + ["<u8"] * 3 + ["<f8", "<f8", "<u8", "<f8", "<u8"],
     "offsets": [0, 4, 8, 12, 16, 20, 24, 28, 32, 36, 40, 44, 48, 52, 56, 60,
-                64, 72, 80, 88, 96, 104, 112],
+                64, 72, 80, 88, 96, 104, 112, 120],
     "itemsize": 128,
 })
 

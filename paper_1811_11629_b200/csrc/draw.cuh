@@ -16,7 +16,7 @@ namespace rsa {
 // (q = 2^63-25, p1, p2 in (2^31, 2^32), lcg skip).
 struct FastInst {
     uint32_t p1, p2, p1_inv, p2_inv, a, k1, k2, garner, r2_1, r2_2, e;
-    double n_float, n_recip;
+    double p2d, n_float, n_recip, n_recip_lo;
 };
 
 RSA_DEV FastInst load_fast(const rsa_instance* __restrict__ ip) {
@@ -26,12 +26,16 @@ RSA_DEV FastInst load_fast(const rsa_instance* __restrict__ ip) {
     P.p1 = w0.x; P.p2 = w0.y; P.p1_inv = w0.z; P.p2_inv = w0.w;
     P.a = w1.x; P.e = w1.y; P.k1 = w1.z; P.k2 = w1.w;
     P.r2_1 = w2.x; P.r2_2 = w2.y; P.garner = w2.z;
+    P.p2d = (double)P.p2;
     P.n_float = __ldg(&ip->n_float);
     P.n_recip = __ldg(&ip->n_recip);
+    P.n_recip_lo = __ldg(&ip->n_recip_lo);
     return P;
 }
 
-// Lane state in registers: skip s (< q) and scaled messages x = m*R^-1 mod p.
+// Lane state in registers: skip s (< q) and canonical scaled messages
+// x = m R^-1 mod p.  (Lazy [0, 2^32) representatives and a word-level skip were
+// measured 1-3 % slower on B200 — profiles/r01_ab_variants.txt.)
 struct Lane {
     uint64_t s;
     uint32_t x1, x2;
@@ -54,19 +58,26 @@ RSA_DEV uint32_t pow_e(uint32_t x, uint32_t e, uint32_t p, uint32_t pinv) {
     else return pow_runtime(x, e, p, pinv);
 }
 
-// One draw on the fast path; returns c in [0, n).
+// One draw on the fast path: advances the lane and returns (h, c2) with the
+// ciphertext c = h*p2 + c2, h = (c1 - c2)*p2inv mod p1 (Garner).
 template <uint32_t E>
-RSA_DEV uint64_t draw_fast(const FastInst& P, Lane& L) {
+RSA_DEV void draw_fast_hc(const FastInst& P, Lane& L, uint32_t& h, uint32_t& c2) {
     L.s = skip_q63(L.s, P.a);
     L.x1 = add_mod(L.x1, mont_redc(L.s, P.p1, P.p1_inv), P.p1);
     L.x2 = add_mod(L.x2, mont_redc(L.s, P.p2, P.p2_inv), P.p2);
     uint32_t y1 = pow_e<E>(L.x1, P.e, P.p1, P.p1_inv);   // m1^e R^-(2e-1)
     uint32_t y2 = pow_e<E>(L.x2, P.e, P.p2, P.p2_inv);
     uint32_t c1 = mont_mul(y1, P.k1, P.p1, P.p1_inv);    // m1^e mod p1
-    uint32_t c2 = mont_mul(y2, P.k2, P.p2, P.p2_inv);    // m2^e mod p2
+    c2 = mont_mul(y2, P.k2, P.p2, P.p2_inv);             // m2^e mod p2
     uint32_t c2r = c2 >= P.p1 ? c2 - P.p1 : c2;          // c2 < 2^32 < 2 p1
     uint32_t d = sub_mod(c1, c2r, P.p1);
-    uint32_t h = mont_mul(d, P.garner, P.p1, P.p1_inv);  // d * p2inv mod p1
+    h = mont_mul(d, P.garner, P.p1, P.p1_inv);           // d * p2inv mod p1
+}
+
+template <uint32_t E>
+RSA_DEV uint64_t draw_fast(const FastInst& P, Lane& L) {
+    uint32_t h, c2;
+    draw_fast_hc<E>(P, L, h, c2);
     return (uint64_t)h * P.p2 + c2;
 }
 
@@ -75,7 +86,7 @@ RSA_DEV uint64_t draw_fast(const FastInst& P, Lane& L) {
 struct GenInst {
     uint32_t p1, p2, p1_inv, p2_inv, a, e, k1, k2, r2_1, r2_2, garner, q1, q2, mode;
     uint64_t q, n;
-    double n_float, n_recip;
+    double n_float, n_recip, n_recip_lo;
 };
 
 RSA_DEV GenInst load_gen(const rsa_instance* __restrict__ ip) {
@@ -85,6 +96,7 @@ RSA_DEV GenInst load_gen(const rsa_instance* __restrict__ ip) {
     G.r2_1 = ip->r2_1; G.r2_2 = ip->r2_2; G.garner = ip->garner;
     G.q1 = ip->q1; G.q2 = ip->q2; G.mode = ip->skip_mode;
     G.q = ip->q; G.n = ip->n; G.n_float = ip->n_float; G.n_recip = ip->n_recip;
+    G.n_recip_lo = ip->n_recip_lo;
     return G;
 }
 

@@ -28,6 +28,9 @@ RSA_DEV void store_f64(double* p, const double (&v)[LPT]) {
 }
 
 // Fast path: E = compile-time exponent (0 = runtime e), LPT lanes per thread.
+// On B200 IMAD.WIDE / IMAD.HI (2 slots) and FP64 ops (1 slot) share one
+// 64-slot/clk/SM datapath (profiles/r01_probe_hybrid.txt): a Montgomery
+// product costs 5 slots, a REDC 3, the skip 6, the float map 5.
 template <uint32_t E, int LPT, bool RAW, bool F64>
 __global__ void __launch_bounds__(256)
 k_fill_fast(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t total_lanes,
@@ -51,7 +54,7 @@ k_fill_fast(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t total_l
         if constexpr (F64) {
             double r[LPT];
 #pragma unroll
-            for (int j = 0; j < LPT; ++j) r[j] = to_unit(c[j], P.n_float, P.n_recip);
+            for (int j = 0; j < LPT; ++j) r[j] = to_unit(c[j], P.n_float, P.n_recip, P.n_recip_lo);
             store_f64<LPT>(f64 + off, r);
         }
     }
@@ -83,7 +86,7 @@ k_fill_general(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t tota
     for (uint64_t k = 0; k < blocks; ++k, off += mv) {
         uint64_t c = draw_general(G, L);
         if (raw) raw[off] = c;
-        if (f64) f64[off] = to_unit(c, G.n_float, G.n_recip);
+        if (f64) f64[off] = to_unit(c, G.n_float, G.n_recip, G.n_recip_lo);
     }
     m1[lane] = mont_mul(L.x1, G.r2_1, G.p1, G.p1_inv);
     m2[lane] = mont_mul(L.x2, G.r2_2, G.p2, G.p2_inv);
@@ -94,9 +97,10 @@ __global__ void k_floats_from_raw(const uint64_t* __restrict__ raw, uint64_t cou
                                   double* __restrict__ out) {
     double nf = __ull2double_rn(n);
     double nr = __drcp_rn(nf);
+    double nl = __dmul_rn(__fma_rn(-nf, nr, 1.0), nr);
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count;
          j += (uint64_t)gridDim.x * blockDim.x)
-        out[j] = to_unit(raw[j], nf, nr);
+        out[j] = to_unit(raw[j], nf, nr, nl);
 }
 
 // (hi*2^64 + lo) mod p for p < 2^32.
@@ -189,10 +193,11 @@ extern "C" int rsa_fill(const rsa_instance* inst, uint32_t n_inst, uint32_t mv, 
     if (n_inst > 1 && (raw_out || f64_out) && inst_stride < blocks * (uint64_t)mv) return RSA_EINVAL;
     if (blocks == 0) return RSA_OK;
     cudaStream_t st = as_stream(stream);
-    if (flags & RSA_FLAG_FAST) {
+    if ((flags & RSA_FLAG_FAST) && !(flags & RSA_FLAG_GENERAL_PATH)) {
         // two lanes per thread needs even mv and 16-byte aligned output rows
         bool pair = (mv % 2 == 0) && (n_inst == 1 || inst_stride % 2 == 0) &&
-                    ((uintptr_t)raw_out % 16 == 0) && ((uintptr_t)f64_out % 16 == 0);
+                    ((uintptr_t)raw_out % 16 == 0) && ((uintptr_t)f64_out % 16 == 0) &&
+                    !(flags & RSA_FLAG_ONE_LANE);
         if (pair)
             dispatch_e<2>(e, grid_for(lanes / 2, 256), st, inst, mv, lanes, blocks, m1, m2, s, raw_out, f64_out, inst_stride);
         else

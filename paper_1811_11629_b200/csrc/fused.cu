@@ -5,7 +5,8 @@
 // (stats.py:118-136)).
 //
 // One thread = one Mv=1 instance (rsacore.take_floats semantics,
-// rsacore.py:261-264).  Per draw, beyond the fill path: 1 DADD + 3 DFMA for the
+// rsacore.py:261-264), drawn by draw.cuh's fast path (the fill kernels' draw).
+// Per draw, beyond the fill path: 1 DADD + 3 DFMA for the
 // moments/lag/pair sums, 2 SHFL for the partner stream (adjacent lanes hold
 // instances 2j, 2j+1), 1 DFMA(rz) for the bin, and a u16 shared-memory counter
 // bump (flushed to the u32 global row every 2^15 draws so it cannot wrap).
@@ -49,7 +50,7 @@ k_fused(const rsa_instance* __restrict__ inst, uint32_t n_inst, uint64_t draws,
 
     double s1 = 0.0, s2 = 0.0, lag = 0.0, xy = 0.0, prev = 0.0, first = 0.0;
     for (uint64_t k = 0; k < draws; ++k) {
-        double r = to_unit(draw_fast<E>(P, L), P.n_float, P.n_recip);
+        double r = to_unit(draw_fast<E>(P, L), P.n_float, P.n_recip, P.n_recip_lo);
         first = k == 0 ? r : first;
         s1 += r;
         s2 = __fma_rn(r, r, s2);

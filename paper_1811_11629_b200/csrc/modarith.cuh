@@ -145,25 +145,28 @@ RSA_DEV uint64_t skip_schrage(uint64_t s, uint64_t a, uint64_t q, uint64_t q1, u
 
 constexpr double MAX_BELOW_ONE = 0x1.fffffffffffffp-1;  // rsacore.py:30
 
-// RN(x / N) given y = RN(1/N), without the hardware divide sequence.
-// q0 = RN(x*y) is within 1.5 ulp of x/N; one residual step r = x - q0*N (FMA),
-// q1 = RN(q0 + r*y) makes it faithful (within 1 ulp); a second step is then
-// Markstein's correctly rounded final iteration (y within 1/2 ulp of 1/N, q1
-// faithful => RN(q1 + (x - q1 N) y) == RN(x/N)).  x >= 0, N > 0 normal; no
-// underflow/overflow at our magnitudes (x, N < 2^64).  Verified against
-// __ddiv_rn by the GPU tests.
-RSA_DEV double div_rn(double x, double N, double y) {
-    double q = __dmul_rn(x, y);
+// RN(x / N) given y = RN(1/N) and y_lo = RN((1 - N y) y), so y + y_lo = 1/N
+// to ~2^-105 relative.  q0 = RN(x y + RN(x y_lo)) is then within 1/2 ulp +
+// 2^-104 |x/N| of x/N, i.e. faithful, and Markstein's final iteration
+// RN(q0 + (x - q0 N) y) (y within 1/2 ulp of 1/N, q0 faithful, residual exact
+// by FMA) is the correctly rounded quotient.  4 FP64 instructions instead of
+// __ddiv_rn's ~16-slot sequence.  x >= 0, N > 0 normal, no under/overflow at
+// our magnitudes (x, N < 2^64).  Checked bit-exact against IEEE division by
+// tests/test_gpu_fill.py::test_clamp_and_float_map.
+RSA_DEV double div_rn(double x, double N, double y, double y_lo) {
+    double q = __fma_rn(x, y, __dmul_rn(x, y_lo));
     double r = __fma_rn(-q, N, x);
-    q = __fma_rn(r, y, q);
-    r = __fma_rn(-q, N, x);
     return __fma_rn(r, y, q);
 }
 
 // r = min(fl(c)/fl(n), MAX_BELOW_ONE)  (vecgen.py:103-107)
-RSA_DEV double to_unit(uint64_t c, double n_float, double n_recip) {
-    double r = div_rn(__ull2double_rn(c), n_float, n_recip);
+RSA_DEV double unit_from_fl(double x, double n_float, double n_recip, double n_recip_lo) {
+    double r = div_rn(x, n_float, n_recip, n_recip_lo);
     return r < 1.0 ? r : MAX_BELOW_ONE;
+}
+
+RSA_DEV double to_unit(uint64_t c, double n_float, double n_recip, double n_recip_lo) {
+    return unit_from_fl(__ull2double_rn(c), n_float, n_recip, n_recip_lo);
 }
 
 // ---- primality (setup kernels) --------------------------------------------------

@@ -6,21 +6,21 @@
 // (paramfactory.py:195-219, an outward scan of 11-mod-12 positions).
 //
 // Scan: every safe prime above 7 is 11 mod 12, so the candidate sequence is
-// {5, 7} u {first + 12 j}.  Pass 1 tests 8192 consecutive candidates per CTA
-// (one per thread per iteration), packs the verdicts into warp ballots (one
-// u32 word per 32 candidates) and counts them; pass 2 scans the per-CTA counts;
-// pass 3 re-reads the bitmask and writes the primes in ascending order.  Only
-// 1 bit per candidate touches memory, so the scan is bound by the Miller-Rabin
-// IMAD work, not HBM.
+// {5, 7} u {first + 12 j}.  Pass 1 decides 4096 consecutive candidates per CTA
+// in three compacted stages (see k_scan_flags) into a bitmask (one u32 word
+// per 32 candidates) plus a per-CTA count; pass 2 scans the counts; pass 3
+// re-reads the bitmask and writes the primes in ascending order.  Only 1 bit
+// per candidate touches memory, so the scan is bound by the Miller-Rabin IMAD
+// work, not HBM.
 #include "common.cuh"
 #include "modarith.cuh"
 
 namespace rsa {
 
 constexpr int SCAN_BLOCK = 256;
-constexpr int SCAN_ITERS = 32;
-constexpr uint64_t SCAN_PER_CTA = (uint64_t)SCAN_BLOCK * SCAN_ITERS;  // 8192 candidates
-constexpr int WORDS_PER_CTA = (int)(SCAN_PER_CTA / 32);                  // 256
+constexpr int SCAN_ITERS = 16;
+constexpr uint64_t SCAN_PER_CTA = (uint64_t)SCAN_BLOCK * SCAN_ITERS;  // 4096 candidates
+constexpr int WORDS_PER_CTA = (int)(SCAN_PER_CTA / 32);                  // 128
 
 // n is divisible by odd l  <=>  n * l^-1 mod 2^32 <= floor((2^32-1)/l)
 struct DivTest {
@@ -37,27 +37,54 @@ __constant__ DivTest c_div[23] = {DT(5),  DT(7),  DT(11), DT(13), DT(17), DT(19)
                                   DT(67), DT(71), DT(73), DT(79), DT(83), DT(89), DT(97)};
 #undef DT
 
+// branch-free: no early exit, so a warp never waits on its slowest lane here
 RSA_DEV bool has_small_factor(uint32_t n) {
+    bool f = false;
 #pragma unroll
-    for (int i = 0; i < 23; ++i)
-        if (n * c_div[i].inv <= c_div[i].lim) return true;
+    for (int i = 0; i < 23; ++i) f |= n * c_div[i].inv <= c_div[i].lim;
+    return f;
+}
+
+// 2^32 mod n for odd n in (2^29, 2^32): 2^32 - k n with k = floor(2^32 / n) <= 7
+RSA_DEV uint32_t r_mod(uint32_t n) {
+    uint64_t r = (1ull << 32) % n;
+    return (uint32_t)r;
+}
+
+// Strong probable prime to base 2 (numtheory.py:60-78): left-to-right powering
+// in the Montgomery domain where "multiply by 2" is a modular doubling, so the
+// 31-bit exponent costs only squarings.
+RSA_DEV bool sprp2(uint32_t n) {
+    const uint32_t ninv = inv32(n), onem = r_mod(n);
+    uint32_t d = n - 1;
+    const int u = __ffs(d) - 1;
+    d >>= u;
+    uint32_t x = onem;  // 1 in Montgomery form
+    for (int b = 31 - __clz(d); b >= 0; --b) {
+        x = mont_mul(x, x, n, ninv);
+        if ((d >> b) & 1u) x = add_mod(x, x, n);
+    }
+    const uint32_t minus1 = n - onem;
+    if (x == onem || x == minus1) return true;
+    for (int j = 1; j < u; ++j) {
+        x = mont_mul(x, x, n, ninv);
+        if (x == minus1) return true;
+    }
     return false;
 }
 
-RSA_DEV bool mr_2_7_61(uint32_t n) {
-    uint32_t ninv = inv32(n);
-    uint32_t onem = (uint32_t)((1ull << 32) % n);
+RSA_DEV bool mr_7_61(uint32_t n) {
+    uint32_t ninv = inv32(n), onem = r_mod(n);
     uint32_t r2 = (uint32_t)(((uint64_t)onem * onem) % n);
-    return sprp32(n, 2, ninv, onem, r2) && sprp32(n, 7, ninv, onem, r2) &&
-           sprp32(n, 61, ninv, onem, r2);
+    return sprp32(n, 7, ninv, onem, r2) && sprp32(n, 61, ninv, onem, r2);
 }
 
-// Safe-prime predicate for a scan candidate (5, 7, or p = 11 mod 12).
+// Safe-prime predicate for one scan candidate (5, 7, or p = 11 mod 12).
 RSA_DEV bool candidate_is_safe(uint32_t p) {
     if (p < 10201u) return is_safe_prime32(p);  // small: exact generic path
     uint32_t q = (p - 1) >> 1;                   // odd, not divisible by 3
     if (has_small_factor(p) || has_small_factor(q)) return false;
-    return mr_2_7_61(p) && mr_2_7_61(q);
+    return sprp2(p) && sprp2(q) && mr_7_61(p) && mr_7_61(q);
 }
 
 struct ScanRange {
@@ -71,28 +98,74 @@ RSA_DEV uint32_t cand_at(const ScanRange& R, uint64_t j) {
     return j < R.nspec ? R.spec[j] : (uint32_t)(R.first + 12ull * (j - R.nspec));
 }
 
+// Pass 1: verdicts for SCAN_PER_CTA consecutive candidates as a bitmask, in
+// three in-CTA stages so no warp idles on a divergent tail: (a) branch-free
+// trial division of p and (p-1)/2 by 5..97 (candidates are already 11 mod 12),
+// survivors (~11 %) compacted into shared memory; (b) base-2 SPRP on p for the
+// survivors, passers (~15 %) compacted again; (c) bases 7, 61 on p and
+// 2, 7, 61 on (p-1)/2.  Deterministic for n < 4,759,123,141.
 __global__ void __launch_bounds__(SCAN_BLOCK)
 k_scan_flags(ScanRange R, uint32_t* __restrict__ words, uint32_t* __restrict__ cta_counts) {
-    __shared__ uint32_t warp_cnt[SCAN_BLOCK / 32];
+    __shared__ uint32_t flags[WORDS_PER_CTA];
+    __shared__ uint16_t list_a[SCAN_PER_CTA], list_b[SCAN_PER_CTA];
+    __shared__ uint32_t na, nb, total;
     const uint64_t base = (uint64_t)blockIdx.x * SCAN_PER_CTA;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t cnt = 0;
-    for (int it = 0; it < SCAN_ITERS; ++it) {
-        uint64_t j = base + (uint64_t)it * SCAN_BLOCK + threadIdx.x;
-        bool ok = j < R.total && candidate_is_safe(cand_at(R, j));
-        uint32_t bal = __ballot_sync(0xffffffffu, ok);
-        if (lane == 0) {
-            words[j >> 5] = bal;
-            cnt += __popc(bal);
-        }
-    }
-    if (lane == 0) warp_cnt[warp] = cnt;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < WORDS_PER_CTA) flags[threadIdx.x] = 0;
+    if (threadIdx.x == 0) { na = 0; nb = 0; total = 0; }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t t = 0;
-        for (int w = 0; w < SCAN_BLOCK / 32; ++w) t += warp_cnt[w];
-        cta_counts[blockIdx.x] = t;
+    // (a) trial division; small candidates (p < 10201) are decided exactly here
+    for (int it = 0; it < SCAN_ITERS; ++it) {
+        const uint32_t off = it * SCAN_BLOCK + threadIdx.x;
+        const uint64_t j = base + off;
+        bool keep = false;
+        if (j < R.total) {
+            const uint32_t c = cand_at(R, j);
+            if (c < 10201u) {
+                if (is_safe_prime32(c)) atomicOr(&flags[off >> 5], 1u << (off & 31));
+            } else {
+                keep = !has_small_factor(c) && !has_small_factor((c - 1) >> 1);
+            }
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        uint32_t pos = 0;
+        if (lane == 0 && bal) pos = atomicAdd(&na, __popc(bal));
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        if (keep) list_a[pos + __popc(bal & ((1u << lane) - 1))] = (uint16_t)off;
     }
+    __syncthreads();
+    // (b) base-2 SPRP on p
+    const uint32_t n_a = na;
+    for (uint32_t i0 = 0; i0 < n_a; i0 += SCAN_BLOCK) {
+        const uint32_t i = i0 + threadIdx.x;
+        bool keep = false;
+        uint32_t off = 0;
+        if (i < n_a) {
+            off = list_a[i];
+            keep = sprp2(cand_at(R, base + off));
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        uint32_t pos = 0;
+        if (lane == 0 && bal) pos = atomicAdd(&nb, __popc(bal));
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        if (keep) list_b[pos + __popc(bal & ((1u << lane) - 1))] = (uint16_t)off;
+    }
+    __syncthreads();
+    // (c) remaining witnesses
+    const uint32_t n_b = nb;
+    for (uint32_t i = threadIdx.x; i < n_b; i += SCAN_BLOCK) {
+        const uint32_t off = list_b[i];
+        const uint32_t p = cand_at(R, base + off), q = (p - 1) >> 1;
+        if (sprp2(q) && mr_7_61(p) && mr_7_61(q)) atomicOr(&flags[off >> 5], 1u << (off & 31));
+    }
+    __syncthreads();
+    if (threadIdx.x < WORDS_PER_CTA) {
+        const uint32_t w = flags[threadIdx.x];
+        words[blockIdx.x * (uint64_t)WORDS_PER_CTA + threadIdx.x] = w;
+        atomicAdd(&total, __popc(w));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) cta_counts[blockIdx.x] = total;
 }
 
 // Exclusive scan of the per-CTA counts (single CTA, chunked, deterministic).

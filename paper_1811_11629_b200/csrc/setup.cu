@@ -74,7 +74,8 @@ RSA_DEV void build_instance(rsa_instance* o, uint32_t p1, uint32_t p2, uint32_t 
     v.b = mulmod64(q % n, ((q - 1) >> 1) % n, n);  // q(q-1)/2 mod n, q odd
     v.n_float = __ull2double_rn(n);
     v.n_recip = __drcp_rn(v.n_float);
-    v.skip_const = 0; v.reserved2[0] = 0; v.reserved2[1] = 0;
+    v.n_recip_lo = __dmul_rn(__fma_rn(-v.n_float, v.n_recip, 1.0), v.n_recip);
+    v.skip_const = 0; v.reserved2 = 0;
     *o = v;
 }
 

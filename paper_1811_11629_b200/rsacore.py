@@ -182,8 +182,17 @@ def _instance_record(params: GeneratorParams) -> np.ndarray:
     r["n"], r["q"], r["b"] = params.n, sk.q, params.b
     r["n_float"] = float(params.n)
     r["n_recip"] = 1.0 / float(params.n)
+    r["n_recip_lo"] = recip_lo(r["n_float"], r["n_recip"])
     r["skip_const"] = params.skip_const
     return rec
+
+
+def recip_lo(nf: float, y: float) -> float:
+    """RN(RN(1 - nf*y) * y) with the inner residual exact (as the device's
+    fma(-nf, y, 1) computes it): the low half of 1/nf ~ y + y_lo."""
+    from fractions import Fraction
+    e = float(1 - Fraction(nf) * Fraction(y))       # exactly representable
+    return float(Fraction(e) * Fraction(y))          # single rounding
 
 
 @functools.lru_cache(maxsize=256)

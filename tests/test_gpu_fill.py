@@ -256,3 +256,53 @@ def test_take_into_host_buffer(p0):
     dev = R.take_floats(b, n)
     assert torch.equal(host, dev.cpu())
     assert torch.equal(a._pending, b._pending) and a.draws == b.draws
+
+
+def _fill_with(pe, flags, mv, blocks, m0, raw=True, f64=True):
+    from paper_1811_11629_b200 import _device
+    d = torch.device("cuda")
+    inst = rsacore.device_instance(pe, d)
+    m1, m2, s = vecgen._init_lanes(inst, 1, mv, m0 % pe.n, 1, d)
+    s0 = u64np(s).copy()
+    r = torch.empty(blocks * mv, dtype=torch.uint64, device=d) if raw else None
+    f = torch.empty(blocks * mv, dtype=torch.float64, device=d) if f64 else None
+    _lib.call("rsa_fill", inst.data_ptr(), 1, mv, blocks, pe.e, flags, m1.data_ptr(), m2.data_ptr(),
+              s.data_ptr(), r.data_ptr() if raw else None, f.data_ptr() if f64 else None, blocks * mv,
+              _device.stream(d))
+    return (u64np(r) if raw else None, u64np(f) if f64 else None,
+            (u64np(m1), u64np(m2), u64np(s)), s0)
+
+
+@pytest.mark.parametrize("e", [3, 5, 7, 9, 17, 257, 65537])
+def test_fast_equals_general_path(p0, golden_meta, e):
+    """The specialised fast kernel (lazy Montgomery, FMA float map, 2 or 1 lanes
+    per thread) and the general kernel (plain %-reductions) agree bit-for-bit
+    on every raw value, double and final lane state, and both match the C
+    oracle on sampled lanes (specialised and runtime exponents)."""
+    pe = dataclasses.replace(p0, e=e)
+    mv, blocks, m0 = 1 << 16, 64, golden_meta["seeded_m0"]
+    rh, fh, sh, s0 = _fill_with(pe, _lib.RSA_FLAG_FAST, mv, blocks, m0)
+    for extra in (_lib.RSA_FLAG_GENERAL_PATH, _lib.RSA_FLAG_ONE_LANE):
+        ri, fi, si, _ = _fill_with(pe, _lib.RSA_FLAG_FAST | extra, mv, blocks, m0)
+        assert np.array_equal(rh, ri) and np.array_equal(fh, fi)
+        for a, b in zip(sh, si):
+            assert np.array_equal(a, b)
+    # f64-only and raw-only variants take different code paths
+    _, f_only, _, _ = _fill_with(pe, _lib.RSA_FLAG_FAST, mv, blocks, m0, raw=False)
+    r_only, _, _, _ = _fill_with(pe, _lib.RSA_FLAG_FAST, mv, blocks, m0, f64=False)
+    assert np.array_equal(f_only, fh) and np.array_equal(r_only, rh)
+    lanes = np.unique(np.random.default_rng(e).integers(0, mv, size=200))
+    cp = coracle.params(pe.p1, pe.p2, e, pe.skip.a)
+    k = len(lanes)
+    want_r, want_f = coracle.fill(cp, np.full(k, m0 % pe.p1, dtype=np.uint64),
+                                  np.full(k, m0 % pe.p2, dtype=np.uint64), s0[lanes].copy(), blocks)
+    assert np.array_equal(rh.reshape(blocks, mv)[:, lanes], want_r)
+    assert np.array_equal(fh.reshape(blocks, mv)[:, lanes], want_f)
+
+
+def test_odd_lane_counts_take_the_scalar_store_path(p0):
+    for mv in (1, 3, 33, 65):
+        a = R.init_vector(p0, mv=mv)
+        got = u64np(R.take_floats(a, mv * 50))
+        st = O.init(O.Params(p0.p1, p0.p2, p0.e, p0.skip.a), mv=mv)
+        assert np.array_equal(got, O.take_floats(st, mv * 50))

@@ -1,0 +1,44 @@
+"""Count fmaheavy-pipe slots per loop iteration from cuobjdump -sass text.
+
+    python tools/sass_slots.py <sass.txt> [start_line end_line]
+
+Weights from tools/probe_*.cu measurements on B200: IMAD.WIDE / IMAD.HI = 2
+slots, other IMAD forms = 1, FP64 ops (DFMA, DMUL, DADD, DSETP, DMNMX) = 1 on
+the same 64-slot/clk/SM datapath."""
+import re
+import sys
+from collections import Counter
+
+lines = open(sys.argv[1]).read().splitlines()
+if len(sys.argv) > 3:
+    lines = lines[int(sys.argv[2]) - 1:int(sys.argv[3])]
+else:
+    # the hot loop: from the target of the last backward BRA.U to that branch
+    idx = [i for i, l in enumerate(lines) if re.search(r"BRA\.U +UP0, 0x([0-9a-f]+)", l)]
+    i1 = idx[-1]
+    tgt = re.search(r"BRA\.U +UP0, 0x([0-9a-f]+)", lines[i1]).group(1)
+    i0 = next(i for i, l in enumerate(lines) if re.search(r"/\*0*%s\*/" % tgt.lstrip("0"), l))
+    lines = lines[i0:i1 + 1]
+ops = Counter()
+heavy = 0.0
+alu = 0
+total = 0
+for l in lines:
+    m = re.search(r"\*/\s+(?:@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]*)", l)
+    if not m:
+        continue
+    op = m.group(1)
+    total += 1
+    ops[op] += 1
+    base = op.split(".")[0]
+    if op.startswith("IMAD.WIDE") or op.startswith("IMAD.HI"):
+        heavy += 2
+    elif base == "IMAD":
+        heavy += 1
+    elif base in ("DFMA", "DMUL", "DADD", "DSETP", "DMNMX"):
+        heavy += 1
+    elif base in ("IADD3", "LOP3", "SEL", "ISETP", "SHF", "LEA", "FSEL", "VIADD", "IABS", "PRMT", "MOV", "IMNMX", "VIMNMX"):
+        alu += 1
+print(f"instructions {total}  heavy slots {heavy}  alu {alu}")
+for k, v in ops.most_common():
+    print(f"  {v:4d} {k}")
