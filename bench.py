@@ -84,7 +84,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={','.join(self.FIELDS)}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -281,6 +281,7 @@ def run_config2(args, world, rank, local):
     elapsed = t0.elapsed_time(t1) * 1e-3
     elapsed_max = max_over_ranks(elapsed, world)
     per_e = {e: statistics.mean(a.elapsed_time(b) * 1e-3 for a, b in ev[e]) for e in EXPONENTS}
+    clk_summary = clk.summary()
     total_numbers = world * args.steps * len(EXPONENTS) * count
     value = total_numbers / elapsed_max / 1e9
 
@@ -300,6 +301,7 @@ def run_config2(args, world, rank, local):
                 "hbm": {"achieved_gbs": 8 * count / per_e[dom] / 1e9, "peak_gbs": hbm_peak,
                         "frac": (8 * count / per_e[dom] / 1e9 / hbm_peak) if hbm_peak else None,
                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)"},
+                "heavy_pipe": heavy_pipe(f"fill_e{dom}", count, per_e[dom], peak, clk_summary),
                 "per_exponent": {str(e): {"ms": per_e[e] * 1e3, "gnumbers_s": count / per_e[e] / 1e9,
                                           "imad_frac": w_imad(e) * count / per_e[e] / peak["ops_per_s"],
                                           "hbm_frac": (8 * count / per_e[e] / 1e9 / hbm_peak) if hbm_peak else None}
@@ -341,7 +343,7 @@ def run_config2(args, world, rank, local):
                        "mv": MV, "blocks": BLOCKS, "exponents": list(EXPONENTS), "m0": m0,
                        "l2": "outputs 8 GiB per fill (> L2), no flush needed",
                        "parallelism": f"independent instances x{world}"},
-            "roofline": roofline, "clocks": clk.summary(), "gpu_launches": args.steps * len(EXPONENTS),
+            "roofline": roofline, "clocks": clk_summary, "gpu_launches": args.steps * len(EXPONENTS),
             "e2e": e2e, "imad_peak_tops": peak["ops_per_s"] / 1e12}
     return line
 
@@ -354,6 +356,34 @@ def _fill_flags(state, count, out, extra):
     _lib.call("rsa_fill", inst.data_ptr(), 1, state.mv, count // state.mv, p.e,
               _lib.RSA_FLAG_FAST | extra, state.m1.data_ptr(), state.m2.data_ptr(),
               state.s.data_ptr(), None, out.data_ptr(), count, _device.stream(state.device))
+
+
+def load_slots(key: str):
+    try:
+        with open(os.path.join(ROOT, "profiles", "slots.json")) as fh:
+            return json.load(fh).get(key)
+    except (OSError, ValueError):
+        return None
+
+
+def heavy_pipe(key: str, draws: int, seconds: float, peak: dict, clk: dict) -> dict | None:
+    """The datapath that actually bounds the kernel: IMAD.WIDE/IMAD.HI (2
+    slots), IMAD and FP64 ops (1 slot) share 64 slots/clk/SM on B200
+    (profiles/r01_probe_hybrid.txt).  Slots per draw are counted from the SASS
+    (tools/slots_json.py -> profiles/slots.json); the measured peak is the
+    in-run Montgomery-triple probe (3 instructions = 5 slots)."""
+    spd = load_slots(key)
+    if not spd:
+        return None
+    ach = spd * draws / seconds
+    meas = peak["ops_per_s"] * 5.0 / 3.0
+    out = {"slots_per_draw": spd, "achieved_tslots": ach / 1e12, "peak_tslots_measured": meas / 1e12,
+           "frac_of_measured": ach / meas}
+    if clk.get("sm_mhz"):
+        nominal = 64.0 * peak["sms"] * clk["sm_mhz"] * 1e6
+        out["peak_tslots_nominal_at_clock"] = nominal / 1e12
+        out["frac_of_nominal"] = ach / nominal
+    return out
 
 
 def load_traffic(key: str):

@@ -103,9 +103,20 @@ def run_other(args, world, rank, local):
     first, n = shard_range(1 << 20, world, rank)
     paramfactory.safe_prime_table(dev)  # the derivation table (built once, untimed)
 
+    phase = {"scan": [], "setup": []}
+
     def fn():
-        paramfactory.safe_primes_u32(lo, hi, dev)
+        st = torch.cuda.current_stream()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(st)
+        sp = paramfactory.safe_primes_u32(lo, hi, dev)
+        e1.record(st)
         R.derive_params_table(R.DEFAULT_MASTER_SEED, first, n, dev=dev)
+        e2.record(st)
+        e2.synchronize()
+        phase["scan"].append(e0.elapsed_time(e1))
+        phase["setup"].append(e1.elapsed_time(e2))
+        phase["count"] = int(sp.numel())
 
     el, clk = _time_steps(args, world, fn, local)
     cands = (hi_all - lo_all) // 2
@@ -115,4 +126,9 @@ def run_other(args, world, rank, local):
                        "unit_note": "value = odd candidates per second (scan + tuples in the step)"},
                       args.steps * 5)
     line["unit"] = "Gcandidates/s"
+    scan_ms = statistics.median(phase["scan"][-args.steps:])
+    setup_ms = statistics.median(phase["setup"][-args.steps:])
+    line["phases"] = {"scan_ms": scan_ms, "scan_gcandidates_s": cands / world / (scan_ms * 1e-3) / 1e9,
+                      "safe_primes_found": phase["count"], "setup_ms": setup_ms,
+                      "tuples_per_s": n / (setup_ms * 1e-3)}
     return line

@@ -80,7 +80,8 @@ class RsaCudaError(RuntimeError):
 
 
 def lib_path() -> str:
-    return _build.LIB
+    """The in-tree library; RSARAND_B200_LIB overrides it (A/B runs only)."""
+    return os.environ.get("RSARAND_B200_LIB", _build.LIB)
 
 
 def load(build_if_missing: bool = True):

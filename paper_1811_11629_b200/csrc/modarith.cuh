@@ -145,17 +145,22 @@ RSA_DEV uint64_t skip_schrage(uint64_t s, uint64_t a, uint64_t q, uint64_t q1, u
 
 constexpr double MAX_BELOW_ONE = 0x1.fffffffffffffp-1;  // rsacore.py:30
 
-// RN(x / N) given y = RN(1/N) and y_lo = RN((1 - N y) y), so y + y_lo = 1/N
-// to ~2^-105 relative.  q0 = RN(x y + RN(x y_lo)) is then within 1/2 ulp +
-// 2^-104 |x/N| of x/N, i.e. faithful, and Markstein's final iteration
-// RN(q0 + (x - q0 N) y) (y within 1/2 ulp of 1/N, q0 faithful, residual exact
-// by FMA) is the correctly rounded quotient.  4 FP64 instructions instead of
-// __ddiv_rn's ~16-slot sequence.  x >= 0, N > 0 normal, no under/overflow at
-// our magnitudes (x, N < 2^64).  Checked bit-exact against IEEE division by
-// tests/test_gpu_fill.py::test_clamp_and_float_map.
-RSA_DEV double div_rn(double x, double N, double y, double y_lo) {
-    double q = __fma_rn(x, y, __dmul_rn(x, y_lo));
+// RN(x / N) given y = RN(1/N), without the hardware divide sequence.
+// q0 = RN(x*y) is within 1.5 ulp of x/N; one residual step r = x - q0*N (FMA),
+// q1 = RN(q0 + r*y) makes it faithful (within 1 ulp); a second step is then
+// Markstein's correctly rounded final iteration (y within 1/2 ulp of 1/N, q1
+// faithful => RN(q1 + (x - q1 N) y) == RN(x/N)).  x >= 0, N > 0 normal; no
+// underflow/overflow at our magnitudes (x, N < 2^64).  5 FP64-pipe slots
+// against __ddiv_rn's ~16.  (A 4-op variant seeded with the double-double
+// reciprocal y + y_lo is also correctly rounded, but scheduled 3.7 % slower in
+// the e=65537 fill on B200 — profiles/r01_ab_v1_v3.txt — so y_lo is kept in
+// rsa_instance for callers but unused here.)  Checked bit-exact against IEEE
+// division by tests/test_gpu_fill.py::test_clamp_and_float_map.
+RSA_DEV double div_rn(double x, double N, double y, double /*y_lo*/) {
+    double q = __dmul_rn(x, y);
     double r = __fma_rn(-q, N, x);
+    q = __fma_rn(r, y, q);
+    r = __fma_rn(-q, N, x);
     return __fma_rn(r, y, q);
 }
 

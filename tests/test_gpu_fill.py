@@ -306,3 +306,50 @@ def test_odd_lane_counts_take_the_scalar_store_path(p0):
         got = u64np(R.take_floats(a, mv * 50))
         st = O.init(O.Params(p0.p1, p0.p2, p0.e, p0.skip.a), mv=mv)
         assert np.array_equal(got, O.take_floats(st, mv * 50))
+
+
+@pytest.mark.parametrize("mv,stride_pad", [(64, 0), (3, 0), (8, 5), (1, 0)])
+def test_multi_instance_layout(golden_streams, mv, stride_pad):
+    """n_inst > 1 in one launch: instance-major rows out[i*stride + k*mv + g],
+    each row the instance's own stream (odd mv / padded strides take the
+    one-lane path)."""
+    from paper_1811_11629_b200 import _device
+    t = R.derive_params_table(golden_streams["master_seed"], 10, 6)
+    d = t.device
+    blocks = 37
+    stride = blocks * mv + stride_pad
+    m1, m2, s = vecgen._init_lanes(t.inst, 6, mv, 12345, 1, d)
+    out = torch.full((6 * stride,), -1.0, dtype=torch.float64, device=d)
+    raw = torch.zeros(6 * stride, dtype=torch.uint64, device=d)
+    _lib.call("rsa_fill", t.inst.data_ptr(), 6, mv, blocks, 9, _lib.RSA_FLAG_FAST, m1.data_ptr(),
+              m2.data_ptr(), s.data_ptr(), raw.data_ptr(), out.data_ptr(), stride, _device.stream(d))
+    out, raw = u64np(out).reshape(6, stride), u64np(raw).reshape(6, stride)
+    for i in range(6):
+        P = O.from_fields(golden_streams["streams"][str(10 + i)])
+        st = O.init(P, m0=12345, mv=mv)
+        want = O.take_raw(st, blocks * mv)
+        assert np.array_equal(raw[i, :blocks * mv], want)
+        assert np.array_equal(out[i, :blocks * mv], O.floats_from_raw(want, P))
+        assert (out[i, blocks * mv:] == -1.0).all()
+
+
+def test_capi_argument_errors(p0):
+    from paper_1811_11629_b200 import _device
+    lib = _lib.load()
+    d = torch.device("cuda")
+    inst = rsacore.device_instance(p0, d)
+    st = torch.zeros(3 * 8, dtype=torch.uint64, device=d)
+    o = torch.empty(64, dtype=torch.float64, device=d)
+    sp = _device.stream(d)
+    # inst_stride smaller than a row of output for n_inst > 1
+    assert lib.rsa_fill(inst.data_ptr(), 2, 4, 4, 9, 1, st.data_ptr(), st.data_ptr(), st.data_ptr(),
+                        None, o.data_ptr(), 8, sp) == _lib.RSA_EINVAL
+    assert lib.rsa_fill(inst.data_ptr(), 1, 0, 4, 9, 1, st.data_ptr(), st.data_ptr(), st.data_ptr(),
+                        None, o.data_ptr(), 8, sp) == _lib.RSA_EINVAL
+    assert lib.rsa_fused_stats(inst.data_ptr(), 3, 4, 9, st.data_ptr(), st.data_ptr(), st.data_ptr(),
+                               o.data_ptr(), o.data_ptr(), sp) == _lib.RSA_EINVAL
+    # zero blocks is a no-op
+    assert lib.rsa_fill(inst.data_ptr(), 1, 4, 0, 9, 1, st.data_ptr(), st.data_ptr(), st.data_ptr(),
+                        None, o.data_ptr(), 0, sp) == _lib.RSA_OK
+    with pytest.raises(_lib.RsaCudaError):
+        _lib.call("rsa_safe_prime_scan", 0, (1 << 32) + 1, None, 0, st.data_ptr(), None, 0, sp)

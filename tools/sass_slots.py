@@ -13,12 +13,27 @@ lines = open(sys.argv[1]).read().splitlines()
 if len(sys.argv) > 3:
     lines = lines[int(sys.argv[2]) - 1:int(sys.argv[3])]
 else:
-    # the hot loop: from the target of the last backward BRA.U to that branch
-    idx = [i for i, l in enumerate(lines) if re.search(r"BRA\.U +UP0, 0x([0-9a-f]+)", l)]
-    i1 = idx[-1]
-    tgt = re.search(r"BRA\.U +UP0, 0x([0-9a-f]+)", lines[i1]).group(1)
-    i0 = next(i for i, l in enumerate(lines) if re.search(r"/\*0*%s\*/" % tgt.lstrip("0"), l))
-    lines = lines[i0:i1 + 1]
+    # the hot loop: among innermost loops (no backward branch inside), the one
+    # carrying the most heavy slots
+    loops = []
+    for i, l in enumerate(lines):
+        m = re.search(r"/\*([0-9a-f]{4,})\*/.*\bBRA(?:\.U)?\s+(?:!?U?P\w+,\s*)?0x([0-9a-f]+)", l)
+        if m and int(m.group(2), 16) < int(m.group(1), 16):
+            tgt = int(m.group(2), 16)
+            i0 = next(k for k, x in enumerate(lines) if re.search(r"/\*0*%x\*/" % tgt, x))
+            loops.append((i0, i))
+    inner = [(a, b) for a, b in loops if not any(a <= c and d < b and (c, d) != (a, b) for c, d in loops)]
+
+    def weight(span):
+        w = 0
+        for l in lines[span[0]:span[1] + 1]:
+            mm = re.search(r"\*/\s+(?:@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]*)", l)
+            if mm and mm.group(1).startswith(("IMAD", "DFMA", "DMUL")):
+                w += 1
+        return w
+
+    a, b = max(inner, key=weight)
+    lines = lines[a:b + 1]
 ops = Counter()
 heavy = 0.0
 alu = 0
@@ -41,4 +56,4 @@ for l in lines:
         alu += 1
 print(f"instructions {total}  heavy slots {heavy}  alu {alu}")
 for k, v in ops.most_common():
-    print(f"  {v:4d} {k}")
+    print(f"  {v:4d} {k}", flush=True)

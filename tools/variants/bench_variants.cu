@@ -23,6 +23,9 @@ using namespace rsa;
 #ifndef LPT
 #define LPT 2
 #endif
+#ifndef MINB
+#define MINB 1
+#endif
 
 struct C {
     uint32_t p1, p2, i1, i2, a, k1, k2, g;
@@ -95,7 +98,7 @@ RSA_DEV double draw(const C& P, uint64_t& s, uint32_t& x1, uint32_t& x2) {
 }
 
 template <uint32_t E>
-__global__ void __launch_bounds__(256) k(C P, uint32_t mv, uint64_t blocks, uint64_t* s_, uint32_t* m1_,
+__global__ void __launch_bounds__(256, MINB) k(C P, uint32_t mv, uint64_t blocks, uint64_t* s_, uint32_t* m1_,
                                          uint32_t* m2_, double* out) {
     uint64_t lane = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * LPT;
     uint64_t s[LPT];
@@ -108,7 +111,10 @@ __global__ void __launch_bounds__(256) k(C P, uint32_t mv, uint64_t blocks, uint
 #pragma unroll
         for (int j = 0; j < LPT; ++j) r[j] = draw<E>(P, s[j], x1[j], x2[j]);
         if constexpr (LPT == 2) __stcs(reinterpret_cast<double2*>(out + off), make_double2(r[0], r[1]));
-        else __stcs(out + off, r[0]);
+        else if constexpr (LPT == 4) {
+            __stcs(reinterpret_cast<double2*>(out + off), make_double2(r[0], r[1]));
+            __stcs(reinterpret_cast<double2*>(out + off + 2), make_double2(r[2], r[3]));
+        } else __stcs(out + off, r[0]);
     }
 #pragma unroll
     for (int j = 0; j < LPT; ++j) { s_[lane + j] = s[j]; m1_[lane + j] = x1[j]; m2_[lane + j] = x2[j]; }
@@ -171,8 +177,8 @@ int main() {
         kx<<<1184, 256>>>((const uint64_t*)out, (uint64_t)MV * BLOCKS, acc);
         unsigned long long h; cudaMemcpy(&h, acc, 8, cudaMemcpyDeviceToHost);
         double clk = best * 1e-3 * 1.965e9 * 148 / ((double)MV * BLOCKS);
-        printf("ADD=%d SKIP=%d FL=%d DIV=%d CLAMP=%d LPT=%d  e=%-6u %8.3f ms  %.3f SM-clk/draw  chk=%016llx\n",
-               ADD, SKIP, FL, DIV, CLAMP, LPT, E, best, clk, h);
+        printf("MINB=%d ADD=%d SKIP=%d FL=%d DIV=%d CLAMP=%d LPT=%d  e=%-6u %8.3f ms  %.3f SM-clk/draw  chk=%016llx\n",
+               MINB, ADD, SKIP, FL, DIV, CLAMP, LPT, E, best, clk, h);
     }
     printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
