@@ -279,6 +279,40 @@ def gen_derive_all(out, n_ids=1 << 20, procs=None):
         procs=procs, seconds=round(time.time() - t, 1))
 
 
+def gen_streamio(out):
+    """Byte digests of the reference CLI `gen` output (cli.py:131-151)."""
+    import tempfile
+    from rsarand import cli
+    rows = {}
+    with tempfile.TemporaryDirectory() as td:
+        for fmt in ("raw64", "f64le", "text"):
+            for count, lanes, chunkcase in ((5000, 64, "small"), ((1 << 22) + 777, 64, "multi_chunk")):
+                if fmt == "text" and chunkcase == "multi_chunk":
+                    continue
+                path = os.path.join(td, f"{fmt}_{chunkcase}")
+                cli.main(["gen", "--seed", str(SEED), "--stream", "3", "--count", str(count),
+                          "--lanes", str(lanes), "--format", fmt, "--out", path])
+                data = open(path, "rb").read()
+                rows[f"{fmt}_{chunkcase}"] = dict(count=count, lanes=lanes, stream=3, bytes=len(data),
+                                                  sha256=hashlib.sha256(data).hexdigest())
+    out["streamio.json"] = dict(source="rsarand.cli gen --seed DEFAULT --stream 3", cases=rows)
+
+
+def gen_bitsource(out, arrays):
+    """rsarand.stats.BitSource over the interstream protocol of cli.cmd_test
+    (cli.py:162-176): distinct pairs, common multiplier, m0=0, s0=1."""
+    from rsarand import stats
+    first = stream(5)
+    plist = [first] + [stream(5 + j, multiplier=first.skip.a) for j in range(1, 3)]
+    meta = {"streams": [5, 6, 7], "lanes": 16, "takes": [1000, 5000, 3, 333]}
+    for sel in ("float_leading", "raw_low_bits", "raw_word"):
+        for k in (1, 3):
+            src = stats.BitSource([vecgen.init_vector(p, m0=0, s0=1, mv=16) for p in plist[:k]], sel)
+            parts = [src.take(n) for n in meta["takes"]]
+            arrays[f"bitsource_{sel}_{k}"] = np.concatenate(parts)
+    out["bitsource.json"] = meta
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-derive-all", action="store_true")
@@ -296,6 +330,12 @@ def main():
         gen_vectors(arrays, meta)
         np.savez_compressed(os.path.join(HERE, "vectors.npz"), **arrays)
         out["vectors.json"] = meta
+    if not only or "bitsource" in only:
+        arr = {}
+        gen_bitsource(out, arr)
+        np.savez_compressed(os.path.join(HERE, "bitsource.npz"), **arr)
+    if not only or "streamio" in only:
+        gen_streamio(out)
     if (not only or "census" in only) and not args.skip_census:
         gen_census(out)
     if (not only or "derive_all" in only) and not args.skip_derive_all:
