@@ -37,6 +37,24 @@ __constant__ DivTest c_div[23] = {DT(5),  DT(7),  DT(11), DT(13), DT(17), DT(19)
                                   DT(67), DT(71), DT(73), DT(79), DT(83), DT(89), DT(97)};
 #undef DT
 
+// Shared-memory sieve primes 5..251 with 12^-1 and 6^-1 mod l: for the CTA's
+// candidates p_u = P0 + 12u (q_u = Q0 + 6u), l | p_u <=> u == -P0 12^-1 (mod l).
+constexpr int NSIEVE = 52;
+struct SievePrime {
+    uint16_t l, inv12, inv6;
+};
+__constant__ SievePrime c_sieve[NSIEVE] = {
+    {5, 3, 1}, {7, 3, 6}, {11, 1, 2}, {13, 12, 11}, {17, 10, 3}, {19, 8, 16},
+    {23, 2, 4}, {29, 17, 5}, {31, 13, 26}, {37, 34, 31}, {41, 24, 7}, {43, 18, 36},
+    {47, 4, 8}, {53, 31, 9}, {59, 5, 10}, {61, 56, 51}, {67, 28, 56}, {71, 6, 12},
+    {73, 67, 61}, {79, 33, 66}, {83, 7, 14}, {89, 52, 15}, {97, 89, 81}, {101, 59, 17},
+    {103, 43, 86}, {107, 9, 18}, {109, 100, 91}, {113, 66, 19}, {127, 53, 106}, {131, 11, 22},
+    {137, 80, 23}, {139, 58, 116}, {149, 87, 25}, {151, 63, 126}, {157, 144, 131}, {163, 68, 136},
+    {167, 14, 28}, {173, 101, 29}, {179, 15, 30}, {181, 166, 151}, {191, 16, 32}, {193, 177, 161},
+    {197, 115, 33}, {199, 83, 166}, {211, 88, 176}, {223, 93, 186}, {227, 19, 38}, {229, 210, 191},
+    {233, 136, 39}, {239, 20, 40}, {241, 221, 201}, {251, 21, 42},
+};
+
 // branch-free: no early exit, so a warp never waits on its slowest lane here
 RSA_DEV bool has_small_factor(uint32_t n) {
     bool f = false;
@@ -99,32 +117,61 @@ RSA_DEV uint32_t cand_at(const ScanRange& R, uint64_t j) {
 }
 
 // Pass 1: verdicts for SCAN_PER_CTA consecutive candidates as a bitmask, in
-// three in-CTA stages so no warp idles on a divergent tail: (a) branch-free
-// trial division of p and (p-1)/2 by 5..97 (candidates are already 11 mod 12),
-// survivors (~11 %) compacted into shared memory; (b) base-2 SPRP on p for the
-// survivors, passers (~15 %) compacted again; (c) bases 7, 61 on p and
-// 2, 7, 61 on (p-1)/2.  Deterministic for n < 4,759,123,141.
+// three in-CTA stages so no warp idles on a divergent tail: (a) a shared-memory
+// sieve of p and (p-1)/2 by the primes 5..251 (candidates are already 11 mod
+// 12), survivors (~8 %) compacted into shared memory; (b) base-2 SPRP on p for
+// the survivors, passers compacted again; (c) bases 7, 61 on p and 2, 7, 61 on
+// (p-1)/2.  Deterministic for n < 4,759,123,141.
 __global__ void __launch_bounds__(SCAN_BLOCK)
 k_scan_flags(ScanRange R, uint32_t* __restrict__ words, uint32_t* __restrict__ cta_counts) {
     __shared__ uint32_t flags[WORDS_PER_CTA];
     __shared__ uint16_t list_a[SCAN_PER_CTA], list_b[SCAN_PER_CTA];
+    __shared__ uint8_t comp[SCAN_PER_CTA];
+    __shared__ uint16_t start[2 * NSIEVE];
     __shared__ uint32_t na, nb, total;
     const uint64_t base = (uint64_t)blockIdx.x * SCAN_PER_CTA;
     const int lane = threadIdx.x & 31;
+    // the sieve path needs only 11-mod-12 candidates, all >= 10201 (so no
+    // sieving prime divides p or q trivially and MR's bases are below n)
+    const bool sieve = base >= R.nspec && R.first + 12ull * (base - R.nspec) >= 10201u;
     if (threadIdx.x < WORDS_PER_CTA) flags[threadIdx.x] = 0;
     if (threadIdx.x == 0) { na = 0; nb = 0; total = 0; }
+    if (sieve) {
+        for (uint32_t u = threadIdx.x; u < SCAN_PER_CTA; u += SCAN_BLOCK) comp[u] = 0;
+        if (threadIdx.x < 2 * NSIEVE) {
+            const SievePrime sp = c_sieve[threadIdx.x >> 1];
+            const uint64_t P0 = R.first + 12ull * (base - R.nspec);
+            const uint32_t l = sp.l;
+            uint32_t r, inv;
+            if (threadIdx.x & 1) { r = (uint32_t)(((P0 - 1) >> 1) % l); inv = sp.inv6; }
+            else { r = (uint32_t)(P0 % l); inv = sp.inv12; }
+            start[threadIdx.x] = (uint16_t)(((l - r) % l) * inv % l);
+        }
+    }
     __syncthreads();
-    // (a) trial division; small candidates (p < 10201) are decided exactly here
+    if (sieve) {
+        for (int k = 0; k < 2 * NSIEVE; ++k) {
+            const uint32_t l = c_sieve[k >> 1].l;
+            for (uint32_t u = start[k] + l * threadIdx.x; u < SCAN_PER_CTA; u += l * SCAN_BLOCK) comp[u] = 1;
+        }
+        __syncthreads();
+    }
+    // (a) sieve survivors (or, in a CTA holding small candidates, trial
+    // division with small candidates decided exactly)
     for (int it = 0; it < SCAN_ITERS; ++it) {
         const uint32_t off = it * SCAN_BLOCK + threadIdx.x;
         const uint64_t j = base + off;
         bool keep = false;
         if (j < R.total) {
-            const uint32_t c = cand_at(R, j);
-            if (c < 10201u) {
-                if (is_safe_prime32(c)) atomicOr(&flags[off >> 5], 1u << (off & 31));
+            if (sieve) {
+                keep = !comp[off];
             } else {
-                keep = !has_small_factor(c) && !has_small_factor((c - 1) >> 1);
+                const uint32_t c = cand_at(R, j);
+                if (c < 10201u) {
+                    if (is_safe_prime32(c)) atomicOr(&flags[off >> 5], 1u << (off & 31));
+                } else {
+                    keep = !has_small_factor(c) && !has_small_factor((c - 1) >> 1);
+                }
             }
         }
         const uint32_t bal = __ballot_sync(0xffffffffu, keep);
