@@ -18,9 +18,9 @@
 namespace rsa {
 
 constexpr int SCAN_BLOCK = 256;
-constexpr int SCAN_ITERS = 16;
-constexpr uint64_t SCAN_PER_CTA = (uint64_t)SCAN_BLOCK * SCAN_ITERS;  // 4096 candidates
-constexpr int WORDS_PER_CTA = (int)(SCAN_PER_CTA / 32);                  // 128
+constexpr int SCAN_ITERS = 64;
+constexpr uint64_t SCAN_PER_CTA = (uint64_t)SCAN_BLOCK * SCAN_ITERS;  // 16384 candidates
+constexpr int WORDS_PER_CTA = (int)(SCAN_PER_CTA / 32);                  // 512
 
 // n is divisible by odd l  <=>  n * l^-1 mod 2^32 <= floor((2^32-1)/l)
 struct DivTest {
@@ -65,8 +65,36 @@ RSA_DEV bool has_small_factor(uint32_t n) {
 
 // 2^32 mod n for odd n in (2^29, 2^32): 2^32 - k n with k = floor(2^32 / n) <= 7
 RSA_DEV uint32_t r_mod(uint32_t n) {
-    uint64_t r = (1ull << 32) % n;
-    return (uint32_t)r;
+    uint32_t r = 0u - n;  // 2^32 - n
+    while (r >= n) r -= n;
+    return r;
+}
+
+// g R mod n for a small base g by a doubling chain on R mod n (ALU only)
+RSA_DEV uint32_t small_base_m(uint32_t g, uint32_t onem, uint32_t n) {
+    uint32_t x = onem;
+    for (int b = 30 - __clz(g); b >= 0; --b) {
+        x = add_mod(x, x, n);
+        if ((g >> b) & 1u) x = add_mod(x, onem, n);
+    }
+    return x;
+}
+
+// strong probable prime to a small base g (numtheory.py:60-78), Montgomery domain
+RSA_DEV bool sprp_small(uint32_t n, uint32_t g) {
+    const uint32_t ninv = inv32(n), onem = r_mod(n);
+    uint32_t d = n - 1;
+    const int u = __ffs(d) - 1;
+    d >>= u;
+    const uint32_t x = mont_pow_m(small_base_m(g, onem, n), d, onem, n, ninv);
+    const uint32_t minus1 = n - onem;
+    if (x == onem || x == minus1) return true;
+    uint32_t y = x;
+    for (int j = 1; j < u; ++j) {
+        y = mont_mul(y, y, n, ninv);
+        if (y == minus1) return true;
+    }
+    return false;
 }
 
 // Strong probable prime to base 2 (numtheory.py:60-78): left-to-right powering
@@ -91,11 +119,7 @@ RSA_DEV bool sprp2(uint32_t n) {
     return false;
 }
 
-RSA_DEV bool mr_7_61(uint32_t n) {
-    uint32_t ninv = inv32(n), onem = r_mod(n);
-    uint32_t r2 = (uint32_t)(((uint64_t)onem * onem) % n);
-    return sprp32(n, 7, ninv, onem, r2) && sprp32(n, 61, ninv, onem, r2);
-}
+RSA_DEV bool mr_7_61(uint32_t n) { return sprp_small(n, 7) && sprp_small(n, 61); }
 
 // Safe-prime predicate for one scan candidate (5, 7, or p = 11 mod 12).
 RSA_DEV bool candidate_is_safe(uint32_t p) {
@@ -116,28 +140,37 @@ RSA_DEV uint32_t cand_at(const ScanRange& R, uint64_t j) {
     return j < R.nspec ? R.spec[j] : (uint32_t)(R.first + 12ull * (j - R.nspec));
 }
 
-// Pass 1: verdicts for SCAN_PER_CTA consecutive candidates as a bitmask, in
-// three in-CTA stages so no warp idles on a divergent tail: (a) a shared-memory
-// sieve of p and (p-1)/2 by the primes 5..251 (candidates are already 11 mod
-// 12), survivors (~8 %) compacted into shared memory; (b) base-2 SPRP on p for
-// the survivors, passers compacted again; (c) bases 7, 61 on p and 2, 7, 61 on
-// (p-1)/2.  Deterministic for n < 4,759,123,141.
+// Pass 1 (per chunk of SCAN_CHUNK_CTAS x 16384 candidates), four kernels with
+// global compaction between them so every stage runs dense, grid-balanced work:
+//  (a) k_scan_sieve: a shared-memory sieve of p and (p-1)/2 by the primes
+//      5..251 (candidates are already 11 mod 12) writes the CTA's 512 bitmask
+//      words (zero, or the exact verdicts of small candidates) and appends the
+//      survivors (~8 %) to a global list with one atomic per CTA;
+//  (b) k_scan_sprp2<Q=0>: base-2 SPRP on p over that list, passers appended;
+//  (c) k_scan_sprp2<Q=1>: base-2 SPRP on (p-1)/2, passers appended;
+//  (d) k_scan_mr761: bases 7 and 61 on both, verdict bits OR-ed into the
+//      bitmask.  Deterministic for n < 4,759,123,141; the bitmask (hence the
+//      output) does not depend on the append order.
+constexpr uint32_t SCAN_CHUNK_CTAS = 1024;
+
 __global__ void __launch_bounds__(SCAN_BLOCK)
-k_scan_flags(ScanRange R, uint32_t* __restrict__ words, uint32_t* __restrict__ cta_counts) {
+k_scan_sieve(ScanRange R, uint64_t cta0, uint32_t* __restrict__ words, uint32_t* __restrict__ surv,
+             uint32_t* __restrict__ nsurv) {
     __shared__ uint32_t flags[WORDS_PER_CTA];
-    __shared__ uint16_t list_a[SCAN_PER_CTA], list_b[SCAN_PER_CTA];
     __shared__ uint8_t comp[SCAN_PER_CTA];
     __shared__ uint16_t start[2 * NSIEVE];
-    __shared__ uint32_t na, nb, total;
-    const uint64_t base = (uint64_t)blockIdx.x * SCAN_PER_CTA;
-    const int lane = threadIdx.x & 31;
+    __shared__ uint16_t wcnt[SCAN_ITERS][SCAN_BLOCK / 32];  // survivors per (iteration, warp)
+    __shared__ uint32_t gbase;
+    const uint64_t cta = cta0 + blockIdx.x;
+    const uint64_t base = cta * SCAN_PER_CTA;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // the sieve path needs only 11-mod-12 candidates, all >= 10201 (so no
     // sieving prime divides p or q trivially and MR's bases are below n)
     const bool sieve = base >= R.nspec && R.first + 12ull * (base - R.nspec) >= 10201u;
-    if (threadIdx.x < WORDS_PER_CTA) flags[threadIdx.x] = 0;
-    if (threadIdx.x == 0) { na = 0; nb = 0; total = 0; }
+    for (uint32_t w = threadIdx.x; w < WORDS_PER_CTA; w += SCAN_BLOCK) flags[w] = 0;
     if (sieve) {
-        for (uint32_t u = threadIdx.x; u < SCAN_PER_CTA; u += SCAN_BLOCK) comp[u] = 0;
+        uint32_t* c32 = reinterpret_cast<uint32_t*>(comp);
+        for (uint32_t u = threadIdx.x; u < SCAN_PER_CTA / 4; u += SCAN_BLOCK) c32[u] = 0;
         if (threadIdx.x < 2 * NSIEVE) {
             const SievePrime sp = c_sieve[threadIdx.x >> 1];
             const uint64_t P0 = R.first + 12ull * (base - R.nspec);
@@ -156,63 +189,106 @@ k_scan_flags(ScanRange R, uint32_t* __restrict__ words, uint32_t* __restrict__ c
         }
         __syncthreads();
     }
-    // (a) sieve survivors (or, in a CTA holding small candidates, trial
-    // division with small candidates decided exactly)
+    // verdict per candidate: survivor (-> MR) or, in a CTA holding small
+    // candidates, trial division with small candidates decided exactly
+    auto keep_at = [&](uint32_t off) -> bool {
+        const uint64_t j = base + off;
+        if (j >= R.total) return false;
+        if (sieve) return !comp[off];
+        const uint32_t c = cand_at(R, j);
+        if (c < 10201u) {
+            if (is_safe_prime32(c)) atomicOr(&flags[off >> 5], 1u << (off & 31));
+            return false;
+        }
+        return !has_small_factor(c) && !has_small_factor((c - 1) >> 1);
+    };
+    for (int it = 0; it < SCAN_ITERS; ++it) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep_at(it * SCAN_BLOCK + threadIdx.x));
+        if (lane == 0) wcnt[it][warp] = (uint16_t)__popc(bal);
+    }
+    __syncthreads();
+    // exclusive prefix over (iteration, warp) in row-major order, total -> global reservation
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int it = 0; it < SCAN_ITERS; ++it)
+            for (int w = 0; w < SCAN_BLOCK / 32; ++w) { uint32_t c = wcnt[it][w]; wcnt[it][w] = (uint16_t)run; run += c; }
+        gbase = run ? atomicAdd(nsurv, run) : 0;
+    }
+    __syncthreads();
+    for (uint32_t w = threadIdx.x; w < WORDS_PER_CTA; w += SCAN_BLOCK) words[cta * WORDS_PER_CTA + w] = flags[w];
     for (int it = 0; it < SCAN_ITERS; ++it) {
         const uint32_t off = it * SCAN_BLOCK + threadIdx.x;
-        const uint64_t j = base + off;
-        bool keep = false;
-        if (j < R.total) {
-            if (sieve) {
-                keep = !comp[off];
-            } else {
+        const bool k = sieve ? (base + off < R.total && !comp[off]) : false;
+        const uint32_t bal = __ballot_sync(0xffffffffu, sieve ? k : false);
+        if (k) surv[gbase + wcnt[it][warp] + __popc(bal & ((1u << lane) - 1))] = (uint32_t)(base + off);
+    }
+    if (!sieve) {
+        // the (rare) trial-division CTA: recompute verdicts for the append
+        for (int it = 0; it < SCAN_ITERS; ++it) {
+            const uint32_t off = it * SCAN_BLOCK + threadIdx.x;
+            const uint64_t j = base + off;
+            bool k = false;
+            if (j < R.total) {
                 const uint32_t c = cand_at(R, j);
-                if (c < 10201u) {
-                    if (is_safe_prime32(c)) atomicOr(&flags[off >> 5], 1u << (off & 31));
-                } else {
-                    keep = !has_small_factor(c) && !has_small_factor((c - 1) >> 1);
-                }
+                k = c >= 10201u && !has_small_factor(c) && !has_small_factor((c - 1) >> 1);
             }
+            const uint32_t bal = __ballot_sync(0xffffffffu, k);
+            if (k) surv[gbase + wcnt[it][warp] + __popc(bal & ((1u << lane) - 1))] = (uint32_t)j;
         }
-        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-        uint32_t pos = 0;
-        if (lane == 0 && bal) pos = atomicAdd(&na, __popc(bal));
-        pos = __shfl_sync(0xffffffffu, pos, 0);
-        if (keep) list_a[pos + __popc(bal & ((1u << lane) - 1))] = (uint16_t)off;
     }
-    __syncthreads();
-    // (b) base-2 SPRP on p
-    const uint32_t n_a = na;
-    for (uint32_t i0 = 0; i0 < n_a; i0 += SCAN_BLOCK) {
+}
+
+// Append the lanes with keep=true to out[] (one atomic per warp).
+RSA_DEV void append_warp(bool keep, uint32_t v, uint32_t* out, uint32_t* n) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+    uint32_t pos = 0;
+    if (lane == 0 && bal) pos = atomicAdd(n, __popc(bal));
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    if (keep) out[pos + __popc(bal & ((1u << lane) - 1))] = v;
+}
+
+template <int Q>
+__global__ void __launch_bounds__(SCAN_BLOCK)
+k_scan_sprp2(ScanRange R, const uint32_t* __restrict__ in, const uint32_t* __restrict__ nin,
+             uint32_t* __restrict__ out, uint32_t* __restrict__ nout) {
+    const uint32_t n = *nin;
+    const uint32_t stride = gridDim.x * SCAN_BLOCK;
+    for (uint32_t i0 = blockIdx.x * SCAN_BLOCK; i0 < n; i0 += stride) {  // warp-uniform trip count
         const uint32_t i = i0 + threadIdx.x;
+        uint32_t j = 0;
         bool keep = false;
-        uint32_t off = 0;
-        if (i < n_a) {
-            off = list_a[i];
-            keep = sprp2(cand_at(R, base + off));
+        if (i < n) {
+            j = in[i];
+            const uint32_t p = cand_at(R, j);
+            keep = sprp2(Q ? (p - 1) >> 1 : p);
         }
-        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-        uint32_t pos = 0;
-        if (lane == 0 && bal) pos = atomicAdd(&nb, __popc(bal));
-        pos = __shfl_sync(0xffffffffu, pos, 0);
-        if (keep) list_b[pos + __popc(bal & ((1u << lane) - 1))] = (uint16_t)off;
+        append_warp(keep, j, out, nout);
     }
-    __syncthreads();
-    // (c) remaining witnesses
-    const uint32_t n_b = nb;
-    for (uint32_t i = threadIdx.x; i < n_b; i += SCAN_BLOCK) {
-        const uint32_t off = list_b[i];
-        const uint32_t p = cand_at(R, base + off), q = (p - 1) >> 1;
-        if (sprp2(q) && mr_7_61(p) && mr_7_61(q)) atomicOr(&flags[off >> 5], 1u << (off & 31));
+}
+
+__global__ void __launch_bounds__(SCAN_BLOCK)
+k_scan_mr761(ScanRange R, const uint32_t* __restrict__ in, const uint32_t* __restrict__ nin,
+             uint32_t* __restrict__ words) {
+    const uint32_t n = *nin;
+    for (uint32_t i = blockIdx.x * SCAN_BLOCK + threadIdx.x; i < n; i += gridDim.x * SCAN_BLOCK) {
+        const uint32_t j = in[i];
+        const uint32_t p = cand_at(R, j);
+        if (mr_7_61(p) && mr_7_61((p - 1) >> 1)) atomicOr(&words[j >> 5], 1u << (j & 31));
     }
+}
+
+// per-CTA-range population counts of the finished bitmask
+__global__ void __launch_bounds__(WORDS_PER_CTA)
+k_scan_counts(const uint32_t* __restrict__ words, uint32_t* __restrict__ counts) {
+    __shared__ uint32_t tot;
+    if (threadIdx.x == 0) tot = 0;
     __syncthreads();
-    if (threadIdx.x < WORDS_PER_CTA) {
-        const uint32_t w = flags[threadIdx.x];
-        words[blockIdx.x * (uint64_t)WORDS_PER_CTA + threadIdx.x] = w;
-        atomicAdd(&total, __popc(w));
-    }
+    uint32_t c = __popc(words[(uint64_t)blockIdx.x * WORDS_PER_CTA + threadIdx.x]);
+    for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&tot, c);
     __syncthreads();
-    if (threadIdx.x == 0) cta_counts[blockIdx.x] = total;
+    if (threadIdx.x == 0) counts[blockIdx.x] = tot;
 }
 
 // Exclusive scan of the per-CTA counts (single CTA, chunked, deterministic).
@@ -294,13 +370,17 @@ static bool make_range(uint64_t lo, uint64_t hi, ScanRange* R) {
 
 static uint64_t scan_ctas(const ScanRange& R) { return (R.total + SCAN_PER_CTA - 1) / SCAN_PER_CTA; }
 
+static uint64_t chunk_ctas(uint64_t ctas) { return ctas < SCAN_CHUNK_CTAS ? ctas : SCAN_CHUNK_CTAS; }
+
+// scratch: words | counts | offsets | surv | surv2 | 3 counters
 extern "C" uint64_t rsa_safe_prime_scan_scratch_bytes(uint64_t lo, uint64_t hi) {
     ScanRange R;
     if (!make_range(lo, hi, &R)) return 0;
     uint64_t ctas = scan_ctas(R);
     if (ctas == 0) ctas = 1;
     uint64_t words = ctas * WORDS_PER_CTA * 4, counts = ((ctas * 4 + 15) / 16) * 16;
-    return words + counts + ctas * 8;
+    uint64_t lists = 2 * chunk_ctas(ctas) * SCAN_PER_CTA * 4;
+    return words + counts + ctas * 8 + lists + 16;  // 3 counters
 }
 
 extern "C" int rsa_safe_prime_scan(uint64_t lo, uint64_t hi, uint32_t* out, uint64_t out_cap,
@@ -317,15 +397,36 @@ extern "C" int rsa_safe_prime_scan(uint64_t lo, uint64_t hi, uint32_t* out, uint
         if (err != cudaSuccess) { set_last_error("rsa_safe_prime_scan", err); return RSA_ECUDA; }
         return RSA_OK;
     }
+    const uint64_t cc = chunk_ctas(ctas);
     char* p = static_cast<char*>(scratch);
     uint32_t* words = reinterpret_cast<uint32_t*>(p);
     p += ctas * WORDS_PER_CTA * 4;
     uint32_t* counts = reinterpret_cast<uint32_t*>(p);
     p += ((ctas * 4 + 15) / 16) * 16;
     uint64_t* offsets = reinterpret_cast<uint64_t*>(p);
-    k_scan_flags<<<(unsigned)ctas, SCAN_BLOCK, 0, st>>>(R, words, counts);
-    int rc = launch_status("rsa_safe_prime_scan(flags)");
-    if (rc) return rc;
+    p += ctas * 8;
+    uint32_t* surv = reinterpret_cast<uint32_t*>(p);
+    p += cc * SCAN_PER_CTA * 4;
+    uint32_t* surv2 = reinterpret_cast<uint32_t*>(p);
+    p += cc * SCAN_PER_CTA * 4;
+    uint32_t* ctr = reinterpret_cast<uint32_t*>(p);  // survivors, base-2(p) passers, base-2(q) passers
+    const unsigned mr_grid = 148 * 8;
+    int rc;
+    for (uint64_t c0 = 0; c0 < ctas; c0 += cc) {
+        const uint64_t n = ctas - c0 < cc ? ctas - c0 : cc;
+        cudaError_t err = cudaMemsetAsync(ctr, 0, 3 * sizeof(uint32_t), st);
+        if (err != cudaSuccess) { set_last_error("rsa_safe_prime_scan(memset)", err); return RSA_ECUDA; }
+        k_scan_sieve<<<(unsigned)n, SCAN_BLOCK, 0, st>>>(R, c0, words, surv, ctr);
+        if ((rc = launch_status("rsa_safe_prime_scan(sieve)"))) return rc;
+        k_scan_sprp2<0><<<mr_grid, SCAN_BLOCK, 0, st>>>(R, surv, ctr, surv2, ctr + 1);
+        if ((rc = launch_status("rsa_safe_prime_scan(sprp2 p)"))) return rc;
+        k_scan_sprp2<1><<<mr_grid, SCAN_BLOCK, 0, st>>>(R, surv2, ctr + 1, surv, ctr + 2);
+        if ((rc = launch_status("rsa_safe_prime_scan(sprp2 q)"))) return rc;
+        k_scan_mr761<<<mr_grid, SCAN_BLOCK, 0, st>>>(R, surv, ctr + 2, words);
+        if ((rc = launch_status("rsa_safe_prime_scan(mr 7,61)"))) return rc;
+    }
+    k_scan_counts<<<(unsigned)ctas, WORDS_PER_CTA, 0, st>>>(words, counts);
+    if ((rc = launch_status("rsa_safe_prime_scan(counts)"))) return rc;
     k_scan_offsets<<<1, 1024, 0, st>>>(counts, ctas, offsets, count);
     if ((rc = launch_status("rsa_safe_prime_scan(offsets)"))) return rc;
     k_scan_write<<<(unsigned)ctas, WORDS_PER_CTA, 0, st>>>(R, words, offsets, out, out_cap);

@@ -200,6 +200,12 @@ def stream_indices(key: StreamKey, n_a: int = len(MULTIPLIER_TABLE)) -> tuple[in
     return beta % K_P1, beta // (K_P1 * K_P2) % n_a
 
 
+@functools.lru_cache(maxsize=64)
+def _checked_skip(a: int) -> SkipParams:
+    """SkipParams.create(a) (primality of q, a*a <= q, primitive root), once per a."""
+    return SkipParams.create(a)
+
+
 def _exponent_usable(e: int) -> bool:
     """make_params accepts e for production pairs iff e is odd and 3 <= e <= 257
     (gcd(e, (p1-1)(p2-1)) = 1 always holds: (p-1)/2 is a prime > 2^30)."""
@@ -281,10 +287,10 @@ def derive_params_table(master_seed: int, first_id: int, count: int, e: int = rs
     if master_seed < 0 or first_id < 0 or first_id + count > 1 << 64:
         raise ValueError("seed and stream ids must be nonnegative 64-bit values")
     if multiplier is not None:
-        SkipParams.create(multiplier)
+        _checked_skip(multiplier)
     else:
         for a in set(multiplier_table):
-            SkipParams.create(a)
+            _checked_skip(a)
     if not _exponent_usable(e):
         raise DerivationExhausted(f"no valid parameters for exponent e={e}")
     cfg = _setup_config(master_seed, first_id, e, len(multiplier_table), multiplier or 0)
