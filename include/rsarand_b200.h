@@ -200,6 +200,29 @@ int rsa_setup_instances(const rsa_setup_config* cfg, uint64_t count,
                         void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Battery counting (reference stats.py:233-466): integer
+ * cell counts of one chi-square test over a device buffer of variates in
+ * [0, 1) (a BitSource chunk), accumulated (+=) into counts.  The statistic is
+ * formed by the caller from the counts exactly as the reference does.
+ *   RSA_BT_HIST        n values, p1 = bins            (frequency)
+ *   RSA_BT_SERIAL      n d-tuples, p1 = d, p2 = axis  (serial)
+ *   RSA_BT_POKER       n 5-card hands                 (poker, counts[5])
+ *   RSA_BT_MAX_OF_T    n t-tuples, p1 = t, p2 = bins  (max-of-t)
+ *   RSA_BT_PERMUTATION n t-tuples, p1 = t <= 10; *flag = 1 on a tie
+ *   RSA_BT_COLLISION   n trials of 2^14 balls (x20 variates when p1 = 1),
+ *                      counts[collisions] += 1        (collision)
+ * --------------------------------------------------------------------------- */
+#define RSA_BT_HIST 1
+#define RSA_BT_SERIAL 2
+#define RSA_BT_POKER 3
+#define RSA_BT_MAX_OF_T 4
+#define RSA_BT_PERMUTATION 5
+#define RSA_BT_COLLISION 6
+
+int rsa_battery_count(int test, const double* v, uint64_t n, uint32_t p1, uint32_t p2,
+                      unsigned long long* counts, int* flag, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Roofline probe: a dependency-free stream of Montgomery triples
  * (IMAD.WIDE.U32, IMAD, IMAD.WIDE.U32) over `grid` CTAs of 256 threads,
  * `iters` iterations; returns through *ops the IMAD-class instruction count

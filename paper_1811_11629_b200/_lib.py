@@ -28,6 +28,7 @@ RSA_ECAPACITY = -4
 RSA_EALIGN = -5
 
 RSA_SKIP_LCG, RSA_SKIP_UNIT, RSA_SKIP_CONST = 0, 1, 2
+RSA_BT_HIST, RSA_BT_SERIAL, RSA_BT_POKER, RSA_BT_MAX_OF_T, RSA_BT_PERMUTATION, RSA_BT_COLLISION = 1, 2, 3, 4, 5, 6
 RSA_FLAG_FAST, RSA_FLAG_FIXED, RSA_FLAG_GENERAL_PATH, RSA_FLAG_ONE_LANE = 1, 2, 4, 8
 
 # rsa_instance (128 bytes) — field order and offsets mirror the C struct.
@@ -69,6 +70,7 @@ PROTOTYPES = {
     "rsa_setup_instances": (ctypes.c_int, [ctypes.POINTER(SetupConfig), c_u64, c_vp, c_vp, c_u64,
                                            c_vp, c_u64, c_vp, c_vp, c_vp, c_vp]),
     "rsa_probe_imad": (ctypes.c_int, [c_u32, c_u32, c_vp, ctypes.POINTER(ctypes.c_double), c_vp]),
+    "rsa_battery_count": (ctypes.c_int, [ctypes.c_int, c_vp, c_u64, c_u32, c_u32, c_vp, c_vp, c_vp]),
     "rsa_abi_version": (ctypes.c_int, []),
     "rsa_built_arch": (ctypes.c_int, []),
     "rsa_last_error": (ctypes.c_char_p, []),

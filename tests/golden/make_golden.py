@@ -313,6 +313,25 @@ def gen_bitsource(out, arrays):
     out["bitsource.json"] = meta
 
 
+def gen_battery(out):
+    """rsarand.stats.run_battery on interstream sources at a small budget:
+    every core test and low-bit rerun (statistic, dof, p, samples)."""
+    from rsarand import stats
+    first = stream(9)
+    plist = [first] + [stream(9 + j, multiplier=first.skip.a) for j in range(1, 2)]
+    budget = 1 << 23
+
+    def make(sel):
+        return stats.BitSource([vecgen.init_vector(p, m0=0, s0=1, mv=256) for p in plist], sel)
+
+    t = time.time()
+    rep = stats.run_battery(make, budget=budget)
+    out["battery.json"] = dict(
+        source="rsarand.stats.run_battery (2 interleaved streams 9,10, common multiplier, mv=256)",
+        streams=[9, 10], lanes=256, budget=budget,
+        reports=[r.record() for r in rep.reports], errors=rep.errors, seconds=round(time.time() - t, 1))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-derive-all", action="store_true")
@@ -330,6 +349,8 @@ def main():
         gen_vectors(arrays, meta)
         np.savez_compressed(os.path.join(HERE, "vectors.npz"), **arrays)
         out["vectors.json"] = meta
+    if not only or "battery" in only:
+        gen_battery(out)
     if not only or "bitsource" in only:
         arr = {}
         gen_bitsource(out, arr)

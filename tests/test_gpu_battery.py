@@ -1,0 +1,71 @@
+"""F1 chi-square battery on the GPU against the reference's own
+stats.run_battery output on the same interleaved streams
+(tests/golden/battery.json, produced by running the reference)."""
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import paper_1811_11629_b200 as R
+from paper_1811_11629_b200 import bitsource, stats
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _golden():
+    return json.load(open(os.path.join(HERE, "golden", "battery.json")))
+
+
+def test_battery_matches_reference():
+    g = _golden()
+    plist = bitsource.interstream_params(R.DEFAULT_MASTER_SEED, g["streams"][0], len(g["streams"]))
+
+    def make(sel):
+        return bitsource.BitSource([R.init_vector(p, m0=0, s0=1, mv=g["lanes"]) for p in plist], sel)
+
+    rep = stats.run_battery(make, budget=g["budget"])
+    got = {r.name: r.record() for r in rep.reports}
+    assert [list(e) for e in rep.errors] == [list(e) for e in g["errors"]]
+    assert list(got) == [r["name"] for r in g["reports"]]
+    for want in g["reports"]:
+        r = got[want["name"]]
+        assert (r["samples"], r["dof"], r["params"]) == (want["samples"], want["dof"], want["params"]), want["name"]
+        if want["name"] == "fourier":
+            # cuFFT vs pocketfft: coefficients within an ulp of a cell edge may bin differently
+            assert math.isclose(r["statistic"], want["statistic"], rel_tol=1e-3), r
+        else:
+            assert r["statistic"] == want["statistic"], want["name"]
+            assert r["p"] == want["p"], want["name"]
+
+
+def test_degenerate_sources_fail_and_floors():
+    class Const:
+        def take(self, n):
+            return np.full(n, 0.25)
+
+    assert not stats.freq_test(Const(), 1 << 20).pass_1e6
+    with pytest.raises(stats.InsufficientSamples):
+        stats.freq_test(Const(), 1000)
+    with pytest.raises(stats.TieDetected):
+        stats.permutation_test(Const(), 3, 1000)
+    with pytest.raises(ValueError):
+        stats.serial_test(Const(), 7, 1 << 22)
+    # perfectly uniform counter sweep scores chi2 = 0 (stats test_freq, test_serial)
+    sweep = (np.arange(1 << 20) + 0.5) / (1 << 20)
+
+    class Sweep:
+        def take(self, n):
+            return sweep[:n]
+
+    r = stats.freq_test(Sweep(), 1 << 20)
+    assert r.result.statistic == 0.0 and r.result.p_value == 1.0
+
+
+def test_poker_and_collision_tables():
+    assert abs(stats.poker_probabilities().sum() - 1.0) < 1e-15
+    d = stats.collision_distribution(4, 8)
+    assert abs(d.sum() - 1.0) < 1e-12
