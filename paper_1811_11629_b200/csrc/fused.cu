@@ -66,6 +66,7 @@ k_fused(const rsa_instance* __restrict__ inst, uint32_t n_inst, uint64_t draws,
             prev = r;
             kk = 1;
         }
+#pragma unroll 2
         for (; kk < len; ++kk) {
             double r = to_unit(draw_fast<E>(P, L), P.n_float, P.n_recip, P.n_recip_lo);
             s1 += r;
