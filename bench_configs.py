@@ -94,6 +94,37 @@ def run_other(args, world, rank, local):
         line["pooled_correlation"] = box["res"].pooled_correlation(total // 2)
         return line
 
+    if args.config == 6:
+        # F1: the full chi-square battery (13 core tests + 10 low-bit reruns)
+        # on 2 interleaved streams at the reference's DEFAULT_BUDGET (1e8 per test)
+        import time
+        from paper_1811_11629_b200 import bitsource, stats
+        budget = 100_000_000
+        plist = bitsource.interstream_params(R.DEFAULT_MASTER_SEED, 9, 2, dev=dev)
+
+        def make(sel):
+            return bitsource.BitSource([R.init_vector(p, m0=0, s0=1, mv=1 << 16, device=dev)
+                                        for p in plist], sel)
+
+        stats.run_battery(make, budget=1 << 23)  # warm-up (allocator, cuFFT plans)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = stats.run_battery(make, budget=budget)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        variates = sum(r.samples for r in rep.reports)
+        line = _base_line(args, world, variates / el / 1e9, el * args.steps, {"sm_mhz": None},
+                          {"workload": "config6 (F1): stats.run_battery, 23 tests at budget 1e8 each, "
+                                       "2 interleaved streams (9, 10), Mv=2^16"}, None)
+        line["unit"] = "Gvariates/s"
+        line["ms_per_step"] = el * 1e3
+        line["battery"] = {"tests": len(rep.reports), "errors": rep.errors, "all_pass": rep.all_pass,
+                           "n_outside_warn": rep.n_outside_warn,
+                           "records": [r.record() for r in rep.reports]}
+        line["reference_context"] = ("reference run_battery at budget 2^23 took 57.6 s on one CPU core here "
+                                     "(tests/golden/battery.json): 3.35e6 variates/s")
+        return line
+
     # config 5: safe-prime scan of [2^31, 2^32) + 2^20 instance tuples
     from paper_1811_11629_b200 import paramfactory
     lo_all, hi_all = 1 << 31, 1 << 32

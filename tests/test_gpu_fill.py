@@ -353,3 +353,28 @@ def test_capi_argument_errors(p0):
                         None, o.data_ptr(), 0, sp) == _lib.RSA_OK
     with pytest.raises(_lib.RsaCudaError):
         _lib.call("rsa_safe_prime_scan", 0, (1 << 32) + 1, None, 0, st.data_ptr(), None, 0, sp)
+
+
+def test_float_map_many_moduli_and_near_midpoints(golden_streams):
+    """The reciprocal + Markstein float map against IEEE division for 512
+    derived moduli: random ciphertexts and ciphertexts whose quotient sits
+    next to a rounding midpoint (the hardest inputs for a correctly rounded
+    divide)."""
+    from paper_1811_11629_b200 import _device
+    t = R.derive_params_table(golden_streams["master_seed"], 5000, 512)
+    ns = t.records()["n"].astype(np.uint64)
+    rng = np.random.default_rng(99)
+    d = torch.device("cuda")
+    for n in ns[:: 8].tolist() + ns[1:: 8][:8].tolist():
+        c = rng.integers(0, n, size=1 << 16, dtype=np.uint64)
+        # near-midpoints: c ~ (j + 1/2) 2^-53 n for random j in [2^51, 2^53)
+        j = rng.integers(1 << 51, 1 << 53, size=1 << 14, dtype=np.uint64)
+        from fractions import Fraction
+        mids = [int((Fraction(int(k)) + Fraction(1, 2)) * n / (1 << 53)) for k in j[:2048]]
+        c = np.concatenate([c, np.array([m + dd for m in mids for dd in (-1, 0, 1) if 0 <= m + dd < n],
+                                        dtype=np.uint64)])
+        want = np.minimum(c.astype(np.float64) / float(n), rsacore.MAX_BELOW_ONE)
+        ct = torch.from_numpy(c).to(d)
+        out = torch.empty(len(c), dtype=torch.float64, device=d)
+        _lib.call("rsa_floats_from_raw", ct.data_ptr(), len(c), int(n), out.data_ptr(), _device.stream(d))
+        assert np.array_equal(u64np(out), want), n
