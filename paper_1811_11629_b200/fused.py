@@ -94,6 +94,14 @@ def all_reduce_pooled(res: FusedStats, group=None) -> FusedStats:
     """Sum the pooled statistics over the ranks of `group` (one NCCL all-reduce
     each for the 7 doubles and the 64 counts; gloo on CPU tensors works too)."""
     import torch.distributed as dist
-    dist.all_reduce(res.pooled, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(res.pooled_hist, op=dist.ReduceOp.SUM, group=group)
+    if dist.get_backend(group) == "nccl" or res.pooled.device.type == "cpu":
+        dist.all_reduce(res.pooled, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(res.pooled_hist, op=dist.ReduceOp.SUM, group=group)
+        return res
+    # gloo with device tensors: reduce through host copies
+    p, h = res.pooled.cpu(), res.pooled_hist.cpu()
+    dist.all_reduce(p, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+    res.pooled.copy_(p)
+    res.pooled_hist.copy_(h)
     return res
