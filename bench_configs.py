@@ -94,6 +94,37 @@ def run_other(args, world, rank, local):
         line["pooled_correlation"] = box["res"].pooled_correlation(total // 2)
         return line
 
+    if args.config == 1:
+        # config 1: one instance (stream 0), 2^20 draws at Mv = 1 (the scalar
+        # stream), 64 (`rsarand gen` default) and 65536 (`rsarand bench` default)
+        p = R.derive_stream_params(R.StreamKey(R.DEFAULT_MASTER_SEED, 0), dev=dev)
+        count = 1 << 20
+        per_mv = {}
+        stream = torch.cuda.current_stream()
+        for mv in (1, 64, 65536):
+            st = R.init_vector(p, m0=0, s0=1, mv=mv, device=dev)
+            out = torch.empty(count, dtype=torch.float64, device=dev)
+            for _ in range(args.warmup):
+                R.take_floats(st, count, out=out)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            bench.barrier_sync(world)
+            a.record(stream)
+            for _ in range(args.steps):
+                R.take_floats(st, count, out=out)
+            b.record(stream)
+            b.synchronize()
+            per_mv[str(mv)] = {"ms_per_2e20": a.elapsed_time(b) / args.steps,
+                               "gnumbers_s": count * args.steps / (a.elapsed_time(b) * 1e-3) / 1e9}
+        el = sum(v["ms_per_2e20"] for v in per_mv.values()) * 1e-3 * args.steps
+        line = _base_line(args, world, 3 * count * args.steps / el / 1e9, el, {"sm_mhz": None},
+                          {"workload": "config1: stream 0, e=9, 2^20 f64 per take_floats at Mv=1, 64, 65536 "
+                                       "(Mv<2^17 lanes are split across threads: rsa_fill_segmented)"},
+                          args.steps * 3 * 3)
+        line["per_mv"] = per_mv
+        line["reference_context"] = ("reference scalar rsacore.take_raws 2.35 us/draw (4.26e5/s) and "
+                                     "vecgen bench_throughput 1.18e7/s at Mv=65536, one core (SURVEY §6)")
+        return line
+
     if args.config == 6:
         # F1: the full chi-square battery (13 core tests + 10 low-bit reruns)
         # on 2 interleaved streams at the reference's DEFAULT_BUDGET (1e8 per test)

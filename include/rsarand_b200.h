@@ -101,6 +101,20 @@ int rsa_fill(const rsa_instance* inst, uint32_t n_inst, uint32_t mv, uint64_t bl
              uint64_t* raw_out, double* f64_out, uint64_t inst_stride,
              void* stream);
 
+/* K1s: the same fill with every lane split into segments of draws, for lane
+ * counts too small to fill the GPU (the scalar stream, Mv = 64).  The skip is
+ * jumped ahead exactly (s0 * (a^L)^j mod q) and the message prefix sums of the
+ * segments are scanned, so results and final state are bit-identical to
+ * rsa_fill.  Requires RSA_FLAG_FAST and at least one output.
+ * rsa_fill_segments(lanes, blocks) = segments per lane it will use (1 = no
+ * benefit: call rsa_fill); scratch >= rsa_fill_segmented_scratch_bytes. */
+uint64_t rsa_fill_segments(uint64_t lanes, uint64_t blocks);
+uint64_t rsa_fill_segmented_scratch_bytes(uint64_t lanes, uint64_t blocks);
+int rsa_fill_segmented(const rsa_instance* inst, uint32_t n_inst, uint32_t mv, uint64_t blocks,
+                       uint32_t e, uint32_t flags, uint64_t* m1, uint64_t* m2, uint64_t* s,
+                       uint64_t* raw_out, double* f64_out, uint64_t inst_stride,
+                       void* scratch, uint64_t scratch_bytes, void* stream);
+
 /* floats_from_raw (vecgen.py:103-107): out[j] = min(fl(raw[j])/fl(n), 1-2^-53). */
 int rsa_floats_from_raw(const uint64_t* raw, uint64_t count, uint64_t n, double* out,
                         void* stream);

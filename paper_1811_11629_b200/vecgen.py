@@ -82,17 +82,30 @@ def init_vector(params: GeneratorParams, m0: int = 0, s0: int = 1, mv: int = 1,
 
 
 def _fill(state: VectorState, blocks: int, raw: torch.Tensor | None, f64: torch.Tensor | None) -> None:
-    """Advance all lanes `blocks` steps, writing block-major outputs."""
+    """Advance all lanes `blocks` steps, writing block-major outputs.  Few
+    lanes x many blocks (the scalar stream, Mv = 64) take the segmented kernel
+    (rsa_fill_segmented: jump-ahead skip + scanned message sums), which splits
+    every lane across many threads with bit-identical results."""
     if blocks <= 0:
         return
     p = state.params
     d = state.device
     inst = device_instance(p, d)
-    _lib.call("rsa_fill", inst.data_ptr(), 1, state.mv, blocks, p.e, instance_flags(p),
-              state.m1.data_ptr(), state.m2.data_ptr(), state.s.data_ptr(),
-              raw.data_ptr() if raw is not None else None,
-              f64.data_ptr() if f64 is not None else None,
-              blocks * state.mv, _device.stream(d))
+    flags = instance_flags(p)
+    L = _lib.load()
+    out_r = raw.data_ptr() if raw is not None else None
+    out_f = f64.data_ptr() if f64 is not None else None
+    nseg = int(L.rsa_fill_segments(state.mv, blocks))
+    if nseg > 1 and flags & _lib.RSA_FLAG_FAST and (raw is not None or f64 is not None):
+        nbytes = int(L.rsa_fill_segmented_scratch_bytes(state.mv, blocks))
+        scratch = torch.empty(nbytes, dtype=torch.uint8, device=d)
+        _lib.call("rsa_fill_segmented", inst.data_ptr(), 1, state.mv, blocks, p.e, flags,
+                  state.m1.data_ptr(), state.m2.data_ptr(), state.s.data_ptr(), out_r, out_f,
+                  blocks * state.mv, scratch.data_ptr(), nbytes, _device.stream(d))
+    else:
+        _lib.call("rsa_fill", inst.data_ptr(), 1, state.mv, blocks, p.e, flags,
+                  state.m1.data_ptr(), state.m2.data_ptr(), state.s.data_ptr(), out_r, out_f,
+                  blocks * state.mv, _device.stream(d))
     state.draws += blocks * state.mv
 
 

@@ -378,3 +378,33 @@ def test_float_map_many_moduli_and_near_midpoints(golden_streams):
         out = torch.empty(len(c), dtype=torch.float64, device=d)
         _lib.call("rsa_floats_from_raw", ct.data_ptr(), len(c), int(n), out.data_ptr(), _device.stream(d))
         assert np.array_equal(u64np(out), want), n
+
+
+@pytest.mark.parametrize("mv,blocks,e", [(1, 1 << 18, 9), (3, 40000, 5), (64, 20000, 65537), (100, 3000, 7)])
+def test_segmented_fill_equals_lane_fill(p0, mv, blocks, e):
+    """rsa_fill_segmented (lanes split across threads: jump-ahead skip + scanned
+    message sums) is bit-identical to the one-thread-per-lane rsa_fill, outputs
+    and final lane state alike."""
+    from paper_1811_11629_b200 import _device
+    pe = dataclasses.replace(p0, e=e)
+    d = torch.device("cuda")
+    inst = rsacore.device_instance(pe, d)
+    lib = _lib.load()
+    assert lib.rsa_fill_segments(mv, blocks) > 1
+    res = []
+    for seg in (False, True):
+        m1, m2, s = vecgen._init_lanes(inst, 1, mv, 987654321, 1, d)
+        r = torch.empty(blocks * mv, dtype=torch.uint64, device=d)
+        f = torch.empty(blocks * mv, dtype=torch.float64, device=d)
+        if seg:
+            nb = int(lib.rsa_fill_segmented_scratch_bytes(mv, blocks))
+            sc = torch.empty(nb, dtype=torch.uint8, device=d)
+            _lib.call("rsa_fill_segmented", inst.data_ptr(), 1, mv, blocks, e, _lib.RSA_FLAG_FAST,
+                      m1.data_ptr(), m2.data_ptr(), s.data_ptr(), r.data_ptr(), f.data_ptr(),
+                      blocks * mv, sc.data_ptr(), nb, _device.stream(d))
+        else:
+            _lib.call("rsa_fill", inst.data_ptr(), 1, mv, blocks, e, _lib.RSA_FLAG_FAST, m1.data_ptr(),
+                      m2.data_ptr(), s.data_ptr(), r.data_ptr(), f.data_ptr(), blocks * mv, _device.stream(d))
+        res.append([u64np(x) for x in (r, f, m1, m2, s)])
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)
