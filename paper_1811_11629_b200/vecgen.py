@@ -221,3 +221,56 @@ def take_raw(state: VectorState, count: int, out: torch.Tensor | None = None) ->
 def take_floats(state: VectorState, count: int, out: torch.Tensor | None = None) -> torch.Tensor:
     """Exactly count doubles in stream order (vecgen.py:142-144)."""
     return _take(state, count, out, floats=True)
+
+
+# ---------------------------------------------------------------------------
+# checkpoint / resume and period jumps for lane vectors (SURVEY.md §8(f) F4;
+# the reference has these for the scalar state only, rsacore.py:276-417)
+
+def jump_periods(state: VectorState, u: int) -> VectorState:
+    """Advance every lane u full skip periods (u*(q-1) draws each) in O(1):
+    one period leaves the skip unchanged and adds b to the message
+    (rsacore.py:276-289), so the jump is m += u*b on every lane."""
+    from .rsacore import UnsupportedSkipMode
+    p = state.params
+    if p.skip_mode != SKIP_LCG:
+        raise UnsupportedSkipMode(f"jump_periods undefined for {p.skip_mode} mode")
+    if u < 0:
+        raise ValueError("u must be >= 0")
+    if state._pending.numel():
+        raise ValueError("jump_periods needs a block-aligned state (drain the pending values first)")
+    ub1, ub2 = u * p.b % p.p1, u * p.b % p.p2
+    for arr, add, mod in ((state.m1, ub1, p.p1), (state.m2, ub2, p.p2)):
+        v = arr.view(torch.int64)  # residues < 2^32: exact in int64
+        v.add_(add).remainder_(mod)
+    state.draws += state.mv * u * (p.skip.q - 1)
+    return state
+
+
+def snapshot(state: VectorState) -> dict:
+    """Host image of a VectorState: the reference's params text
+    (rsacore.params_to_text) plus the lane arrays, draw count and pending raws."""
+    from .rsacore import params_to_text
+    return {"params": params_to_text(state.params), "mv": state.mv, "draws": state.draws,
+            "m1": state.m1.cpu().numpy().copy(), "m2": state.m2.cpu().numpy().copy(),
+            "s": state.s.cpu().numpy().copy(), "pending": state._pending.cpu().numpy().copy()}
+
+
+def restore(snap: dict, device=None) -> VectorState:
+    """Rebuild a VectorState from snapshot(); re-validates the parameters and
+    the lane residue ranges like rsacore.restore (rsacore.py:393-417)."""
+    import numpy as np
+    from .rsacore import MalformedSnapshot, params_from_text
+    p = params_from_text(snap["params"])
+    mv = int(snap["mv"])
+    arrs = [np.asarray(snap[k], dtype=np.uint64) for k in ("m1", "m2", "s")]
+    if any(a.shape != (mv,) for a in arrs):
+        raise MalformedSnapshot("lane arrays must have mv entries")
+    if (arrs[0] >= p.p1).any() or (arrs[1] >= p.p2).any():
+        raise MalformedSnapshot("message residue outside [0, p)")
+    if p.skip_mode == SKIP_LCG and ((arrs[2] == 0) | (arrs[2] >= p.skip.q)).any():
+        raise MalformedSnapshot("skip outside [1, q)")
+    d = _device.device(device)
+    m1, m2, s = (torch.from_numpy(a.copy()).to(d) for a in arrs)
+    pend = torch.from_numpy(np.asarray(snap["pending"], dtype=np.uint64).copy()).to(d)
+    return VectorState(params=p, mv=mv, m1=m1, m2=m2, s=s, draws=int(snap["draws"]), _pending=pend)

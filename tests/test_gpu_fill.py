@@ -408,3 +408,25 @@ def test_segmented_fill_equals_lane_fill(p0, mv, blocks, e):
         res.append([u64np(x) for x in (r, f, m1, m2, s)])
     for a, b in zip(*res):
         assert np.array_equal(a, b)
+
+
+def test_vector_snapshot_restore_and_jump(p0):
+    a = R.init_vector(p0, mv=16)
+    R.take_raw(a, 16 * 10 + 5)
+    snap = vecgen.snapshot(a)
+    want = u64np(R.take_raw(a, 1000))
+    b = vecgen.restore(snap)
+    assert np.array_equal(u64np(R.take_raw(b, 1000)), want)
+    assert b.draws == a.draws
+    # one period jump = u*b added to every lane message (rsacore.jump_periods per lane)
+    c = R.init_vector(p0, mv=4)
+    seeds = u64np(c.s)
+    vecgen.jump_periods(c, 3)
+    for g in range(4):
+        st = rsacore.GeneratorState(m1=0, m2=0, s=int(seeds[g]))
+        rsacore.jump_periods(st, p0, 3)
+        assert (int(c.m1[g].item()), int(c.m2[g].item())) == (st.m1, st.m2)
+    got = u64np(R.take_raw(c, 4 * 8)).reshape(8, 4)
+    for g in range(4):
+        st = rsacore.GeneratorState(m1=3 * p0.b % p0.p1, m2=3 * p0.b % p0.p2, s=int(seeds[g]))
+        assert got[:, g].tolist() == rsacore.take_raws(st, p0, 8)
