@@ -153,22 +153,25 @@ RSA_DEV uint32_t cand_at(const ScanRange& R, uint64_t j) {
 //      output) does not depend on the append order.
 constexpr uint32_t SCAN_CHUNK_CTAS = 1024;
 
+// SIEVE = true: CTAs whose candidates are all 11 mod 12 and >= 10201 (no
+// sieving prime divides p or q trivially, MR's bases are below n);
+// SIEVE = false: the (at most one or two) leading CTAs of a range that starts
+// low, decided by trial division with small candidates settled exactly.
+// Split into two kernels so the hot sieve kernel stays register-lean.
+template <bool SIEVE>
 __global__ void __launch_bounds__(SCAN_BLOCK)
 k_scan_sieve(ScanRange R, uint64_t cta0, uint32_t* __restrict__ words, uint32_t* __restrict__ surv,
              uint32_t* __restrict__ nsurv) {
     __shared__ uint32_t flags[WORDS_PER_CTA];
-    __shared__ uint8_t comp[SCAN_PER_CTA];
+    __shared__ uint8_t comp[SIEVE ? SCAN_PER_CTA : 4];
     __shared__ uint16_t start[2 * NSIEVE];
     __shared__ uint16_t wcnt[SCAN_ITERS][SCAN_BLOCK / 32];  // survivors per (iteration, warp)
     __shared__ uint32_t gbase;
     const uint64_t cta = cta0 + blockIdx.x;
     const uint64_t base = cta * SCAN_PER_CTA;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // the sieve path needs only 11-mod-12 candidates, all >= 10201 (so no
-    // sieving prime divides p or q trivially and MR's bases are below n)
-    const bool sieve = base >= R.nspec && R.first + 12ull * (base - R.nspec) >= 10201u;
     for (uint32_t w = threadIdx.x; w < WORDS_PER_CTA; w += SCAN_BLOCK) flags[w] = 0;
-    if (sieve) {
+    if constexpr (SIEVE) {
         uint32_t* c32 = reinterpret_cast<uint32_t*>(comp);
         for (uint32_t u = threadIdx.x; u < SCAN_PER_CTA / 4; u += SCAN_BLOCK) c32[u] = 0;
         if (threadIdx.x < 2 * NSIEVE) {
@@ -180,30 +183,31 @@ k_scan_sieve(ScanRange R, uint64_t cta0, uint32_t* __restrict__ words, uint32_t*
             else { r = (uint32_t)(P0 % l); inv = sp.inv12; }
             start[threadIdx.x] = (uint16_t)(((l - r) % l) * inv % l);
         }
-    }
-    __syncthreads();
-    if (sieve) {
+        __syncthreads();
         for (int k = 0; k < 2 * NSIEVE; ++k) {
             const uint32_t l = c_sieve[k >> 1].l;
             for (uint32_t u = start[k] + l * threadIdx.x; u < SCAN_PER_CTA; u += l * SCAN_BLOCK) comp[u] = 1;
         }
-        __syncthreads();
     }
-    // verdict per candidate: survivor (-> MR) or, in a CTA holding small
-    // candidates, trial division with small candidates decided exactly
-    auto keep_at = [&](uint32_t off) -> bool {
+    __syncthreads();
+    // verdict per candidate: sieve survivor, or trial-division survivor with
+    // small candidates decided exactly (their bit set here, not listed)
+    auto keep_at = [&](uint32_t off, bool decide) -> bool {
         const uint64_t j = base + off;
         if (j >= R.total) return false;
-        if (sieve) return !comp[off];
-        const uint32_t c = cand_at(R, j);
-        if (c < 10201u) {
-            if (is_safe_prime32(c)) atomicOr(&flags[off >> 5], 1u << (off & 31));
-            return false;
+        if constexpr (SIEVE) {
+            return !comp[off];
+        } else {
+            const uint32_t c = cand_at(R, j);
+            if (c < 10201u) {
+                if (decide && is_safe_prime32(c)) atomicOr(&flags[off >> 5], 1u << (off & 31));
+                return false;
+            }
+            return !has_small_factor(c) && !has_small_factor((c - 1) >> 1);
         }
-        return !has_small_factor(c) && !has_small_factor((c - 1) >> 1);
     };
     for (int it = 0; it < SCAN_ITERS; ++it) {
-        const uint32_t bal = __ballot_sync(0xffffffffu, keep_at(it * SCAN_BLOCK + threadIdx.x));
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep_at(it * SCAN_BLOCK + threadIdx.x, true));
         if (lane == 0) wcnt[it][warp] = (uint16_t)__popc(bal);
     }
     __syncthreads();
@@ -218,23 +222,9 @@ k_scan_sieve(ScanRange R, uint64_t cta0, uint32_t* __restrict__ words, uint32_t*
     for (uint32_t w = threadIdx.x; w < WORDS_PER_CTA; w += SCAN_BLOCK) words[cta * WORDS_PER_CTA + w] = flags[w];
     for (int it = 0; it < SCAN_ITERS; ++it) {
         const uint32_t off = it * SCAN_BLOCK + threadIdx.x;
-        const bool k = sieve ? (base + off < R.total && !comp[off]) : false;
-        const uint32_t bal = __ballot_sync(0xffffffffu, sieve ? k : false);
+        const bool k = keep_at(off, false);
+        const uint32_t bal = __ballot_sync(0xffffffffu, k);
         if (k) surv[gbase + wcnt[it][warp] + __popc(bal & ((1u << lane) - 1))] = (uint32_t)(base + off);
-    }
-    if (!sieve) {
-        // the (rare) trial-division CTA: recompute verdicts for the append
-        for (int it = 0; it < SCAN_ITERS; ++it) {
-            const uint32_t off = it * SCAN_BLOCK + threadIdx.x;
-            const uint64_t j = base + off;
-            bool k = false;
-            if (j < R.total) {
-                const uint32_t c = cand_at(R, j);
-                k = c >= 10201u && !has_small_factor(c) && !has_small_factor((c - 1) >> 1);
-            }
-            const uint32_t bal = __ballot_sync(0xffffffffu, k);
-            if (k) surv[gbase + wcnt[it][warp] + __popc(bal & ((1u << lane) - 1))] = (uint32_t)j;
-        }
     }
 }
 
@@ -411,13 +401,28 @@ extern "C" int rsa_safe_prime_scan(uint64_t lo, uint64_t hi, uint32_t* out, uint
     p += cc * SCAN_PER_CTA * 4;
     uint32_t* ctr = reinterpret_cast<uint32_t*>(p);  // survivors, base-2(p) passers, base-2(q) passers
     const unsigned mr_grid = 148 * 8;
+    // CTAs [0, small_ctas) hold a special candidate or one below 10201
+    uint64_t small_ctas = 0;
+    while (small_ctas < ctas) {
+        const uint64_t b = small_ctas * SCAN_PER_CTA;
+        if (b >= R.nspec && R.first + 12ull * (b - R.nspec) >= 10201u) break;
+        ++small_ctas;
+    }
     int rc;
     for (uint64_t c0 = 0; c0 < ctas; c0 += cc) {
         const uint64_t n = ctas - c0 < cc ? ctas - c0 : cc;
         cudaError_t err = cudaMemsetAsync(ctr, 0, 3 * sizeof(uint32_t), st);
         if (err != cudaSuccess) { set_last_error("rsa_safe_prime_scan(memset)", err); return RSA_ECUDA; }
-        k_scan_sieve<<<(unsigned)n, SCAN_BLOCK, 0, st>>>(R, c0, words, surv, ctr);
-        if ((rc = launch_status("rsa_safe_prime_scan(sieve)"))) return rc;
+        // leading CTAs holding candidates below 10201 (or 5, 7) take the trial-division kernel
+        const uint64_t nsmall = c0 < small_ctas ? (small_ctas - c0 < n ? small_ctas - c0 : n) : 0;
+        if (nsmall) {
+            k_scan_sieve<false><<<(unsigned)nsmall, SCAN_BLOCK, 0, st>>>(R, c0, words, surv, ctr);
+            if ((rc = launch_status("rsa_safe_prime_scan(trial)"))) return rc;
+        }
+        if (n > nsmall) {
+            k_scan_sieve<true><<<(unsigned)(n - nsmall), SCAN_BLOCK, 0, st>>>(R, c0 + nsmall, words, surv, ctr);
+            if ((rc = launch_status("rsa_safe_prime_scan(sieve)"))) return rc;
+        }
         k_scan_sprp2<0><<<mr_grid, SCAN_BLOCK, 0, st>>>(R, surv, ctr, surv2, ctr + 1);
         if ((rc = launch_status("rsa_safe_prime_scan(sprp2 p)"))) return rc;
         k_scan_sprp2<1><<<mr_grid, SCAN_BLOCK, 0, st>>>(R, surv2, ctr + 1, surv, ctr + 2);
