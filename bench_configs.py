@@ -183,7 +183,7 @@ def run_other(args, world, rank, local):
     el, clk = _time_steps(args, world, fn, local)
     cands = (hi_all - lo_all) // 2
     line = _base_line(args, world, cands * args.steps / el / 1e9, el, clk,
-                      {"workload": "config5 setup: MR(2,7,61) scan of all 2^30 odd candidates in "
+                      {"workload": "config5 setup: safe-prime scan (sieve to 8191, base-2 SPRP, spsp(2) table) of all 2^30 odd candidates in "
                                    "[2^31,2^32) + 2^20 instance tuples (ids 0..2^20-1)",
                        "unit_note": "value = odd candidates per second (scan + tuples in the step)"},
                       args.steps * 5)

@@ -157,8 +157,10 @@ int rsa_fused_pool(const rsa_fused_stat* stats, const uint32_t* hist, uint32_t n
 /* ---------------------------------------------------------------------------
  * K3: safe-prime scan.  Replaces paramfactory.safe_primes_in (paramfactory.py:105-130)
  * and numtheory.is_safe_prime (numtheory.py:96-98) for [lo, hi), hi <= 2^32:
- * writes the ascending safe primes to out[0..*count) (device count).  Primality is
- * deterministic Miller-Rabin with bases (2, 7, 61) after trial division.
+ * writes the ascending safe primes to out[0..*count) (device count).  Primality of p
+ * and (p-1)/2 is exact: a shared-memory sieve by the primes 5..8191, the base-2
+ * strong-probable-prime test, then a lookup in the complete table of the 2314
+ * base-2 strong pseudoprimes below 2^32.
  * scratch must hold rsa_safe_prime_scan_scratch_bytes(lo, hi) bytes.
  * Returns RSA_ECAPACITY (after writing *count) when out_cap is too small.
  * --------------------------------------------------------------------------- */

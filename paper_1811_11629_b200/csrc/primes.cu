@@ -6,14 +6,15 @@
 // (paramfactory.py:195-219, an outward scan of 11-mod-12 positions).
 //
 // Scan: every safe prime above 7 is 11 mod 12, so the candidate sequence is
-// {5, 7} u {first + 12 j}.  Pass 1 decides 4096 consecutive candidates per CTA
-// in three compacted stages (see k_scan_flags) into a bitmask (one u32 word
-// per 32 candidates) plus a per-CTA count; pass 2 scans the counts; pass 3
+// {5, 7} u {first + 12 j}.  Pass 1 decides 16384 consecutive candidates per
+// CTA in three compacted stages (see the comment above SCAN_CHUNK_CTAS) into a
+// bitmask (one u32 word per 32 candidates); pass 2 counts and scans; pass 3
 // re-reads the bitmask and writes the primes in ascending order.  Only 1 bit
-// per candidate touches memory, so the scan is bound by the Miller-Rabin IMAD
+// per candidate touches memory, so the scan is bound by the base-2 SPRP IMAD
 // work, not HBM.
 #include "common.cuh"
 #include "modarith.cuh"
+#include "spsp2_table.inc"
 
 namespace rsa {
 
@@ -54,6 +55,54 @@ __constant__ SievePrime c_sieve[NSIEVE] = {
     {197, 115, 33}, {199, 83, 166}, {211, 88, 176}, {223, 93, 186}, {227, 19, 38}, {229, 210, 191},
     {233, 136, 39}, {239, 20, 40}, {241, 221, 201}, {251, 21, 42},
 };
+
+// Sieve primes 257 .. RSA_SIEVE_MAX, generated at compile time.  Too sparse
+// for the cooperative loop (fewer marks per CTA than threads), so each thread
+// takes whole (prime, p-or-q) entries.  Sieving p and q this far leaves ~0.44x
+// the survivors of the 251 bound, and the base-2 SPRP stages after the sieve
+// cost ~70x more per survivor than a mark.
+#ifndef RSA_SIEVE_MAX
+#define RSA_SIEVE_MAX 8192
+#endif
+constexpr bool cx_is_prime(uint32_t n) {
+    if (n < 2) return false;
+    for (uint32_t f = 2; f * f <= n; ++f)
+        if (n % f == 0) return false;
+    return true;
+}
+constexpr uint32_t cx_powmod(uint32_t b, uint32_t e, uint32_t m) {
+    uint32_t r = 1 % m;
+    b %= m;
+    while (e) {
+        if (e & 1) r = r * b % m;
+        b = b * b % m;
+        e >>= 1;
+    }
+    return r;
+}
+constexpr int cx_count_primes(uint32_t lo, uint32_t hi) {
+    int c = 0;
+    for (uint32_t n = lo; n < hi; ++n) c += cx_is_prime(n);
+    return c;
+}
+constexpr int NBIG = cx_count_primes(257, RSA_SIEVE_MAX);
+struct BigPrime {
+    uint16_t l, inv12, inv6, r32;  // r32 = 2^32 mod l
+};
+struct BigTable {
+    BigPrime e[NBIG];
+};
+constexpr BigTable cx_big_table() {
+    BigTable t{};
+    int k = 0;
+    for (uint32_t n = 257; n < RSA_SIEVE_MAX; ++n)
+        if (cx_is_prime(n))
+            t.e[k++] = BigPrime{(uint16_t)n, (uint16_t)cx_powmod(12, n - 2, n), (uint16_t)cx_powmod(6, n - 2, n),
+                                (uint16_t)((1ull << 32) % n)};
+    return t;
+}
+static_assert(RSA_SIEVE_MAX <= 65536 && RSA_SIEVE_MAX < 10201, "sieve primes must stay below the smallest sieved candidate");
+__device__ const BigTable g_big = cx_big_table();
 
 // branch-free: no early exit, so a warp never waits on its slowest lane here
 RSA_DEV bool has_small_factor(uint32_t n) {
@@ -121,6 +170,50 @@ RSA_DEV bool sprp2(uint32_t n) {
 
 RSA_DEV bool mr_7_61(uint32_t n) { return sprp_small(n, 7) && sprp_small(n, 61); }
 
+// The 2314 base-2 strong pseudoprimes below 2^32 (tools/gen_spsp2.c, which
+// decides compositeness with the deterministic bases 2, 7, 61).  An n < 2^32
+// that is a base-2 SPRP is prime iff it is not in this table, so the scan's
+// last stage is a lookup instead of two more exponentiations.  The table is
+// bucketed at compile time by a multiplicative hash (4096 buckets, at most 4
+// entries each): one load of the bucket bounds, then independent loads of
+// its entries.
+constexpr int SPSP_HASH_BITS = 12, SPSP_NB = 1 << SPSP_HASH_BITS, SPSP_MAXB = 4;
+__host__ __device__ constexpr uint32_t spsp_hash(uint32_t n) { return (n * 0x9E3779B1u) >> (32 - SPSP_HASH_BITS); }
+struct SpspHash {
+    uint16_t start[SPSP_NB + 1];
+    uint32_t v[RSA_SPSP2_COUNT];
+};
+constexpr SpspHash cx_spsp_hash() {
+    const uint32_t tab[RSA_SPSP2_COUNT] = {RSA_SPSP2_TABLE};
+    SpspHash h{};
+    uint16_t fill[SPSP_NB] = {};
+    for (uint32_t k = 0; k < RSA_SPSP2_COUNT; ++k) ++h.start[spsp_hash(tab[k]) + 1];
+    for (int b = 0; b < SPSP_NB; ++b) h.start[b + 1] += h.start[b];
+    for (uint32_t k = 0; k < RSA_SPSP2_COUNT; ++k) {
+        const uint32_t b = spsp_hash(tab[k]);
+        h.v[h.start[b] + fill[b]++] = tab[k];
+    }
+    return h;
+}
+constexpr int cx_spsp_max_bucket(const SpspHash& h) {
+    int m = 0;
+    for (int b = 0; b < SPSP_NB; ++b) m = h.start[b + 1] - h.start[b] > m ? h.start[b + 1] - h.start[b] : m;
+    return m;
+}
+constexpr SpspHash kSpspHash = cx_spsp_hash();
+static_assert(cx_spsp_max_bucket(kSpspHash) <= SPSP_MAXB, "spsp(2) hash bucket overflow");
+__device__ const SpspHash g_spsp = kSpspHash;
+
+RSA_DEV bool is_spsp2(uint32_t n) {
+    const uint32_t b = spsp_hash(n);
+    const uint32_t lo = __ldg(&g_spsp.start[b]), hi = __ldg(&g_spsp.start[b + 1]);
+    bool hit = false;
+#pragma unroll
+    for (uint32_t k = 0; k < SPSP_MAXB; ++k)
+        if (lo + k < hi) hit |= __ldg(&g_spsp.v[lo + k]) == n;
+    return hit;
+}
+
 // Safe-prime predicate for one scan candidate (5, 7, or p = 11 mod 12).
 RSA_DEV bool candidate_is_safe(uint32_t p) {
     if (p < 10201u) return is_safe_prime32(p);  // small: exact generic path
@@ -140,18 +233,30 @@ RSA_DEV uint32_t cand_at(const ScanRange& R, uint64_t j) {
     return j < R.nspec ? R.spec[j] : (uint32_t)(R.first + 12ull * (j - R.nspec));
 }
 
-// Pass 1 (per chunk of SCAN_CHUNK_CTAS x 16384 candidates), four kernels with
+// Pass 1 (per chunk of SCAN_CHUNK_CTAS x 16384 candidates), three kernels with
 // global compaction between them so every stage runs dense, grid-balanced work:
 //  (a) k_scan_sieve: a shared-memory sieve of p and (p-1)/2 by the primes
 //      5..251 (candidates are already 11 mod 12) writes the CTA's 512 bitmask
 //      words (zero, or the exact verdicts of small candidates) and appends the
 //      survivors (~8 %) to a global list with one atomic per CTA;
-//  (b) k_scan_sprp2<Q=0>: base-2 SPRP on p over that list, passers appended;
-//  (c) k_scan_sprp2<Q=1>: base-2 SPRP on (p-1)/2, passers appended;
-//  (d) k_scan_mr761: bases 7 and 61 on both, verdict bits OR-ed into the
-//      bitmask.  Deterministic for n < 4,759,123,141; the bitmask (hence the
-//      output) does not depend on the append order.
-constexpr uint32_t SCAN_CHUNK_CTAS = 1024;
+//  (b) k_scan_sprp2: base-2 SPRP on p over that list, passers appended;
+//  (c) k_scan_final: base-2 SPRP on (p-1)/2, then p and (p-1)/2 must both be
+//      absent from the base-2 strong-pseudoprime table (c_spsp2); verdict bits
+//      OR-ed into the bitmask.  Exact for n < 2^32 (the table is complete
+//      there); the bitmask (hence the output) does not depend on the append
+//      order.
+#ifndef RSA_SCAN_CHUNK_CTAS
+#define RSA_SCAN_CHUNK_CTAS 4096
+#endif
+constexpr uint32_t SCAN_CHUNK_CTAS = RSA_SCAN_CHUNK_CTAS;
+// Capacity of the survivor lists per CTA.  Sieving by 5, 7, 11 and 13 alone
+// leaves exactly 3*5*9*11 = 1485 of every 5*7*11*13 = 5005 consecutive
+// 11-mod-12 candidates (p and (p-1)/2 each avoid one residue class per
+// prime, CRT), so a CTA's 16384 candidates (< 4 periods) hold at most
+// 4 * 1485 = 5940 <= 6144 survivors; the trial-division CTAs test the same
+// primes.  The base-2 passers are a subset.
+constexpr uint64_t LIST_PER_CTA = SCAN_PER_CTA * 3 / 8;
+static_assert(4 * 1485 <= LIST_PER_CTA && SCAN_PER_CTA <= 4 * 5005, "survivor bound");
 
 // SIEVE = true: CTAs whose candidates are all 11 mod 12 and >= 10201 (no
 // sieving prime divides p or q trivially, MR's bases are below n);
@@ -162,18 +267,19 @@ template <bool SIEVE>
 __global__ void __launch_bounds__(SCAN_BLOCK)
 k_scan_sieve(ScanRange R, uint64_t cta0, uint32_t* __restrict__ words, uint32_t* __restrict__ surv,
              uint32_t* __restrict__ nsurv) {
-    __shared__ uint32_t flags[WORDS_PER_CTA];
-    __shared__ uint8_t comp[SIEVE ? SCAN_PER_CTA : 4];
+    __shared__ uint32_t flags[SIEVE ? 1 : WORDS_PER_CTA];
+    __shared__ __align__(16) uint8_t comp[SIEVE ? SCAN_PER_CTA : 4];
     __shared__ uint16_t start[2 * NSIEVE];
-    __shared__ uint16_t wcnt[SCAN_ITERS][SCAN_BLOCK / 32];  // survivors per (iteration, warp)
+    __shared__ uint16_t wcnt[SIEVE ? 1 : SCAN_ITERS][SCAN_BLOCK / 32];  // survivors per (iteration, warp)
     __shared__ uint32_t gbase;
     const uint64_t cta = cta0 + blockIdx.x;
     const uint64_t base = cta * SCAN_PER_CTA;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint32_t w = threadIdx.x; w < WORDS_PER_CTA; w += SCAN_BLOCK) flags[w] = 0;
+    if constexpr (!SIEVE)
+        for (uint32_t w = threadIdx.x; w < WORDS_PER_CTA; w += SCAN_BLOCK) flags[w] = 0;
     if constexpr (SIEVE) {
-        uint32_t* c32 = reinterpret_cast<uint32_t*>(comp);
-        for (uint32_t u = threadIdx.x; u < SCAN_PER_CTA / 4; u += SCAN_BLOCK) c32[u] = 0;
+        uint4* c4z = reinterpret_cast<uint4*>(comp);
+        for (uint32_t u = threadIdx.x; u < SCAN_PER_CTA / 16; u += SCAN_BLOCK) c4z[u] = make_uint4(0, 0, 0, 0);
         if (threadIdx.x < 2 * NSIEVE) {
             const SievePrime sp = c_sieve[threadIdx.x >> 1];
             const uint64_t P0 = R.first + 12ull * (base - R.nspec);
@@ -188,23 +294,75 @@ k_scan_sieve(ScanRange R, uint64_t cta0, uint32_t* __restrict__ words, uint32_t*
             const uint32_t l = c_sieve[k >> 1].l;
             for (uint32_t u = start[k] + l * threadIdx.x; u < SCAN_PER_CTA; u += l * SCAN_BLOCK) comp[u] = 1;
         }
+        {   // large primes: one (prime, p-or-q) entry per thread at a time
+            const uint64_t P0 = R.first + 12ull * (base - R.nspec), Q0 = (P0 - 1) >> 1;
+            for (uint32_t k = threadIdx.x; k < 2u * NBIG; k += SCAN_BLOCK) {
+                const BigPrime bp = g_big.e[k >> 1];
+                const uint32_t l = bp.l;
+                const uint64_t v = (k & 1) ? Q0 : P0;
+                const uint32_t r = ((uint32_t)(v >> 32) * bp.r32 + (uint32_t)v % l) % l;
+                const uint32_t inv = (k & 1) ? bp.inv6 : bp.inv12;
+                for (uint32_t u = (l - r) % l * inv % l; u < SCAN_PER_CTA; u += l) comp[u] = 1;
+            }
+        }
     }
     __syncthreads();
-    // verdict per candidate: sieve survivor, or trial-division survivor with
-    // small candidates decided exactly (their bit set here, not listed)
+    if constexpr (SIEVE) {
+        // candidates past the end of the range count as sieved out
+        const uint64_t valid = R.total > base ? (R.total - base < SCAN_PER_CTA ? R.total - base : SCAN_PER_CTA) : 0;
+        for (uint64_t u = valid + threadIdx.x; u < SCAN_PER_CTA; u += SCAN_BLOCK) comp[u] = 1;
+        __syncthreads();
+        // thread t owns the 16-candidate groups g = i * SCAN_BLOCK + t (i < 4):
+        // conflict-free 128-bit reads, survivors counted as zero bytes
+        const uint4* c4 = reinterpret_cast<const uint4*>(comp);
+        uint32_t w[16], cnt = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint4 v = c4[i * SCAN_BLOCK + threadIdx.x];
+            w[4 * i] = v.x, w[4 * i + 1] = v.y, w[4 * i + 2] = v.z, w[4 * i + 3] = v.w;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) cnt += 4 - __popc(w[i]);
+        // block exclusive scan of the counts -> one global reservation per CTA
+        uint32_t inc = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += o;
+        }
+        __shared__ uint32_t wtot[SCAN_BLOCK / 32];
+        if (lane == 31) wtot[warp] = inc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t run = 0;
+            for (int k = 0; k < SCAN_BLOCK / 32; ++k) { const uint32_t c = wtot[k]; wtot[k] = run; run += c; }
+            gbase = run ? atomicAdd(nsurv, run) : 0;
+        }
+        __syncthreads();
+        uint32_t pos = gbase + wtot[warp] + inc - cnt;
+        for (uint32_t x = threadIdx.x; x < WORDS_PER_CTA; x += SCAN_BLOCK) words[cta * WORDS_PER_CTA + x] = 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            uint32_t z = ~w[i] & 0x01010101u;
+            const uint32_t u0 = 16u * ((i >> 2) * SCAN_BLOCK + threadIdx.x) + 4u * (i & 3);
+            while (z) {
+                surv[pos++] = (uint32_t)(base + u0 + ((__ffs(z) - 1) >> 3));
+                z &= z - 1;
+            }
+        }
+        return;
+    } else {
+    // verdict per candidate: trial-division survivor, small candidates decided
+    // exactly (their bit set here, not listed)
     auto keep_at = [&](uint32_t off, bool decide) -> bool {
         const uint64_t j = base + off;
         if (j >= R.total) return false;
-        if constexpr (SIEVE) {
-            return !comp[off];
-        } else {
-            const uint32_t c = cand_at(R, j);
-            if (c < 10201u) {
-                if (decide && is_safe_prime32(c)) atomicOr(&flags[off >> 5], 1u << (off & 31));
-                return false;
-            }
-            return !has_small_factor(c) && !has_small_factor((c - 1) >> 1);
+        const uint32_t c = cand_at(R, j);
+        if (c < 10201u) {
+            if (decide && is_safe_prime32(c)) atomicOr(&flags[off >> 5], 1u << (off & 31));
+            return false;
         }
+        return !has_small_factor(c) && !has_small_factor((c - 1) >> 1);
     };
     for (int it = 0; it < SCAN_ITERS; ++it) {
         const uint32_t bal = __ballot_sync(0xffffffffu, keep_at(it * SCAN_BLOCK + threadIdx.x, true));
@@ -226,106 +384,212 @@ k_scan_sieve(ScanRange R, uint64_t cta0, uint32_t* __restrict__ words, uint32_t*
         const uint32_t bal = __ballot_sync(0xffffffffu, k);
         if (k) surv[gbase + wcnt[it][warp] + __popc(bal & ((1u << lane) - 1))] = (uint32_t)(base + off);
     }
+    }
 }
 
-// Append the lanes with keep=true to out[] (one atomic per warp).
-RSA_DEV void append_warp(bool keep, uint32_t v, uint32_t* out, uint32_t* n) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-    uint32_t pos = 0;
-    if (lane == 0 && bal) pos = atomicAdd(n, __popc(bal));
-    pos = __shfl_sync(0xffffffffu, pos, 0);
-    if (keep) out[pos + __popc(bal & ((1u << lane) - 1))] = v;
+// K independent base-2 SPRP tests interleaved in one thread.  Each test is a
+// chain of ~31 dependent Montgomery squarings; one chain per thread leaves the
+// IMAD pipe mostly idle (64 warps x 1 chain cannot cover its latency), K
+// chains per thread give the scheduler K-fold ILP.  Leading zero bits of a
+// shorter exponent square the Montgomery one, which stays one, so all K run
+// the same 32-bit-position loop.  Same verdicts as sprp2().
+template <int K>
+RSA_DEV void sprp2_multi(const uint32_t (&n)[K], bool (&ok)[K]) {
+    uint32_t ninv[K], onem[K], d[K], x[K];
+    int u[K];
+    uint32_t dall = 0;
+    int umax = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        ninv[k] = inv32(n[k]);
+        onem[k] = r_mod(n[k]);
+        d[k] = n[k] - 1;
+        u[k] = __ffs(d[k]) - 1;
+        d[k] >>= u[k];
+        x[k] = onem[k];
+        dall |= d[k];
+        umax = max(umax, u[k]);
+    }
+    for (int b = 31 - __clz(dall); b >= 0; --b) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            x[k] = mont_mul(x[k], x[k], n[k], ninv[k]);
+            if ((d[k] >> b) & 1u) x[k] = add_mod(x[k], x[k], n[k]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) ok[k] = x[k] == onem[k] || x[k] == n[k] - onem[k];
+    for (int j = 1; j < umax; ++j) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            x[k] = mont_mul(x[k], x[k], n[k], ninv[k]);
+            ok[k] = ok[k] || (j < u[k] && x[k] == n[k] - onem[k]);
+        }
+    }
 }
 
-template <int Q>
+#ifndef RSA_SPRP_ILP
+#define RSA_SPRP_ILP 2
+#endif
+constexpr int SPRP_ILP = RSA_SPRP_ILP;
+constexpr uint32_t SPRP_DUMMY = 4294967291u;  // a prime: padding lanes stay well-formed
+
+// (b) base-2 SPRP on p over the sieve survivors, passers appended
 __global__ void __launch_bounds__(SCAN_BLOCK)
 k_scan_sprp2(ScanRange R, const uint32_t* __restrict__ in, const uint32_t* __restrict__ nin,
              uint32_t* __restrict__ out, uint32_t* __restrict__ nout) {
     const uint32_t n = *nin;
-    const uint32_t stride = gridDim.x * SCAN_BLOCK;
-    for (uint32_t i0 = blockIdx.x * SCAN_BLOCK; i0 < n; i0 += stride) {  // warp-uniform trip count
-        const uint32_t i = i0 + threadIdx.x;
-        uint32_t j = 0;
-        bool keep = false;
-        if (i < n) {
-            j = in[i];
-            const uint32_t p = cand_at(R, j);
-            keep = sprp2(Q ? (p - 1) >> 1 : p);
+    const uint32_t tile = SPRP_ILP * SCAN_BLOCK, stride = gridDim.x * tile;
+    for (uint32_t i0 = blockIdx.x * tile; i0 < n; i0 += stride) {  // warp-uniform trip count
+        uint32_t j[SPRP_ILP], v[SPRP_ILP];
+        bool ok[SPRP_ILP];
+#pragma unroll
+        for (int k = 0; k < SPRP_ILP; ++k) {
+            const uint32_t i = i0 + k * SCAN_BLOCK + threadIdx.x;
+            j[k] = i < n ? in[i] : 0;
+            v[k] = i < n ? cand_at(R, j[k]) : SPRP_DUMMY;
         }
-        append_warp(keep, j, out, nout);
+        sprp2_multi<SPRP_ILP>(v, ok);
+        // one reservation per warp for all SPRP_ILP groups
+        const int lane = threadIdx.x & 31;
+        uint32_t bal[SPRP_ILP], tot = 0;
+#pragma unroll
+        for (int k = 0; k < SPRP_ILP; ++k) {
+            ok[k] = ok[k] && i0 + k * SCAN_BLOCK + threadIdx.x < n;
+            bal[k] = __ballot_sync(0xffffffffu, ok[k]);
+            tot += __popc(bal[k]);
+        }
+        uint32_t pos = 0;
+        if (lane == 0 && tot) pos = atomicAdd(nout, tot);
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        const uint32_t below = (1u << lane) - 1;
+#pragma unroll
+        for (int k = 0; k < SPRP_ILP; ++k) {
+            if (ok[k]) out[pos + __popc(bal[k] & below)] = j[k];
+            pos += __popc(bal[k]);
+        }
     }
 }
 
+// (c) base-2 SPRP on q = (p-1)/2, then both p and q looked up in the
+// pseudoprime table; verdict bits OR-ed into the bitmask
 __global__ void __launch_bounds__(SCAN_BLOCK)
-k_scan_mr761(ScanRange R, const uint32_t* __restrict__ in, const uint32_t* __restrict__ nin,
+k_scan_final(ScanRange R, const uint32_t* __restrict__ in, const uint32_t* __restrict__ nin,
              uint32_t* __restrict__ words) {
     const uint32_t n = *nin;
-    for (uint32_t i = blockIdx.x * SCAN_BLOCK + threadIdx.x; i < n; i += gridDim.x * SCAN_BLOCK) {
-        const uint32_t j = in[i];
-        const uint32_t p = cand_at(R, j);
-        if (mr_7_61(p) && mr_7_61((p - 1) >> 1)) atomicOr(&words[j >> 5], 1u << (j & 31));
+    const uint32_t tile = SPRP_ILP * SCAN_BLOCK, stride = gridDim.x * tile;
+    for (uint32_t i0 = blockIdx.x * tile; i0 < n; i0 += stride) {
+        uint32_t j[SPRP_ILP], q[SPRP_ILP];
+        bool ok[SPRP_ILP];
+#pragma unroll
+        for (int k = 0; k < SPRP_ILP; ++k) {
+            const uint32_t i = i0 + k * SCAN_BLOCK + threadIdx.x;
+            j[k] = i < n ? in[i] : 0;
+            q[k] = i < n ? (cand_at(R, j[k]) - 1) >> 1 : SPRP_DUMMY;
+        }
+        sprp2_multi<SPRP_ILP>(q, ok);
+#pragma unroll
+        for (int k = 0; k < SPRP_ILP; ++k) {
+            if (ok[k] && i0 + k * SCAN_BLOCK + threadIdx.x < n && !is_spsp2(q[k]) && !is_spsp2(2 * q[k] + 1))
+                atomicOr(&words[j[k] >> 5], 1u << (j[k] & 31));
+        }
     }
 }
 
-// per-CTA-range population counts of the finished bitmask
-__global__ void __launch_bounds__(WORDS_PER_CTA)
-k_scan_counts(const uint32_t* __restrict__ words, uint32_t* __restrict__ counts) {
-    __shared__ uint32_t tot;
-    if (threadIdx.x == 0) tot = 0;
+// Tail of the scan: per-range (16384 candidates = 512 bitmask words) counts,
+// their exclusive scan, and the ordered write.  128 threads x one uint4 cover
+// a range; CTAs loop over ranges so the ~11k ranges of a full 2^31 scan run
+// as one resident wave instead of 11k tiny CTAs.
+constexpr int TAIL_BLOCK = WORDS_PER_CTA / 4;
+static_assert(TAIL_BLOCK == 128, "one uint4 of the bitmask per thread");
+
+RSA_DEV uint32_t block_excl_scan128(uint32_t c, uint32_t* total, uint32_t* smem4) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+    }
+    if (lane == 31) smem4[warp] = incl;
     __syncthreads();
-    uint32_t c = __popc(words[(uint64_t)blockIdx.x * WORDS_PER_CTA + threadIdx.x]);
-    for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
-    if ((threadIdx.x & 31) == 0) atomicAdd(&tot, c);
-    __syncthreads();
-    if (threadIdx.x == 0) counts[blockIdx.x] = tot;
+    uint32_t before = 0, all = 0;
+#pragma unroll
+    for (int k = 0; k < TAIL_BLOCK / 32; ++k) {
+        const uint32_t t = smem4[k];
+        before += k < warp ? t : 0;
+        all += t;
+    }
+    __syncthreads();  // smem4 reusable by the next range
+    *total = all;
+    return before + incl - c;
 }
 
-// Exclusive scan of the per-CTA counts (single CTA, chunked, deterministic).
+__global__ void __launch_bounds__(TAIL_BLOCK)
+k_scan_counts(const uint32_t* __restrict__ words, uint64_t ranges, uint32_t* __restrict__ counts) {
+    __shared__ uint32_t wsum[TAIL_BLOCK / 32];
+    for (uint64_t r = blockIdx.x; r < ranges; r += gridDim.x) {
+        const uint4 v = reinterpret_cast<const uint4*>(words + r * WORDS_PER_CTA)[threadIdx.x];
+        uint32_t tot;
+        block_excl_scan128(__popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w), &tot, wsum);
+        if (threadIdx.x == 0) counts[r] = tot;
+    }
+}
+
+// Exclusive scan of the per-range counts (single CTA, deterministic).
 __global__ void __launch_bounds__(1024)
 k_scan_offsets(const uint32_t* __restrict__ counts, uint64_t n, uint64_t* __restrict__ offsets,
                uint64_t* __restrict__ total) {
-    __shared__ uint64_t part[1024];
+    __shared__ uint64_t wsum[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t per = (n + 1023) / 1024;
     const uint64_t b = threadIdx.x * per, e = min(n, b + per);
     uint64_t sum = 0;
     for (uint64_t i = b; i < e; ++i) sum += counts[i];
-    part[threadIdx.x] = sum;
+    uint64_t incl = sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint64_t run = 0;
-        for (int t = 0; t < 1024; ++t) { uint64_t v = part[t]; part[t] = run; run += v; }
-        *total = run;
+    if (warp == 0) {
+        uint64_t x = wsum[lane], xi = x;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint64_t v = __shfl_up_sync(0xffffffffu, xi, d);
+            if (lane >= d) xi += v;
+        }
+        wsum[lane] = xi - x;
+        if (lane == 31) *total = xi;
     }
     __syncthreads();
-    uint64_t run = part[threadIdx.x];
+    uint64_t run = wsum[warp] + incl - sum;
     for (uint64_t i = b; i < e; ++i) { offsets[i] = run; run += counts[i]; }
 }
 
-__global__ void __launch_bounds__(WORDS_PER_CTA)
-k_scan_write(ScanRange R, const uint32_t* __restrict__ words, const uint64_t* __restrict__ offsets,
-             uint32_t* __restrict__ out, uint64_t out_cap) {
-    __shared__ uint32_t warp_tot[WORDS_PER_CTA / 32];
-    const uint64_t w = (uint64_t)blockIdx.x * WORDS_PER_CTA + threadIdx.x;
-    const uint32_t bits = words[w];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t c = __popc(bits), incl = c;
+__global__ void __launch_bounds__(TAIL_BLOCK)
+k_scan_write(ScanRange R, const uint32_t* __restrict__ words, uint64_t ranges,
+             const uint64_t* __restrict__ offsets, uint32_t* __restrict__ out, uint64_t out_cap) {
+    __shared__ uint32_t wsum[TAIL_BLOCK / 32];
+    for (uint64_t r = blockIdx.x; r < ranges; r += gridDim.x) {
+        const uint4 v = reinterpret_cast<const uint4*>(words + r * WORDS_PER_CTA)[threadIdx.x];
+        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan128(__popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w), &tot, wsum);
+        uint64_t pos = offsets[r] + ex;
+        const uint64_t j0 = r * SCAN_PER_CTA + 128ull * threadIdx.x;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += v;
-    }
-    if (lane == 31) warp_tot[warp] = incl;
-    __syncthreads();
-    uint32_t before = 0;
-    for (int k = 0; k < warp; ++k) before += warp_tot[k];
-    uint64_t pos = offsets[blockIdx.x] + before + incl - c;
-    uint32_t b = bits;
-    while (b) {
-        int bit = __ffs(b) - 1;
-        b &= b - 1;
-        if (pos < out_cap) out[pos] = cand_at(R, w * 32 + bit);
-        ++pos;
+        for (int k = 0; k < 4; ++k) {
+            uint32_t bits = w4[k];
+            while (bits) {
+                const int bit = __ffs(bits) - 1;
+                bits &= bits - 1;
+                if (pos < out_cap) out[pos] = cand_at(R, j0 + 32 * k + bit);
+                ++pos;
+            }
+        }
     }
 }
 
@@ -362,15 +626,15 @@ static uint64_t scan_ctas(const ScanRange& R) { return (R.total + SCAN_PER_CTA -
 
 static uint64_t chunk_ctas(uint64_t ctas) { return ctas < SCAN_CHUNK_CTAS ? ctas : SCAN_CHUNK_CTAS; }
 
-// scratch: words | counts | offsets | surv | surv2 | 3 counters
+// scratch: words | counts | offsets | surv | surv2 | counters
 extern "C" uint64_t rsa_safe_prime_scan_scratch_bytes(uint64_t lo, uint64_t hi) {
     ScanRange R;
     if (!make_range(lo, hi, &R)) return 0;
     uint64_t ctas = scan_ctas(R);
     if (ctas == 0) ctas = 1;
     uint64_t words = ctas * WORDS_PER_CTA * 4, counts = ((ctas * 4 + 15) / 16) * 16;
-    uint64_t lists = 2 * chunk_ctas(ctas) * SCAN_PER_CTA * 4;
-    return words + counts + ctas * 8 + lists + 16;  // 3 counters
+    uint64_t lists = 2 * chunk_ctas(ctas) * LIST_PER_CTA * 4;
+    return words + counts + ctas * 8 + lists + 16;  // counters
 }
 
 extern "C" int rsa_safe_prime_scan(uint64_t lo, uint64_t hi, uint32_t* out, uint64_t out_cap,
@@ -396,11 +660,11 @@ extern "C" int rsa_safe_prime_scan(uint64_t lo, uint64_t hi, uint32_t* out, uint
     uint64_t* offsets = reinterpret_cast<uint64_t*>(p);
     p += ctas * 8;
     uint32_t* surv = reinterpret_cast<uint32_t*>(p);
-    p += cc * SCAN_PER_CTA * 4;
+    p += cc * LIST_PER_CTA * 4;
     uint32_t* surv2 = reinterpret_cast<uint32_t*>(p);
-    p += cc * SCAN_PER_CTA * 4;
-    uint32_t* ctr = reinterpret_cast<uint32_t*>(p);  // survivors, base-2(p) passers, base-2(q) passers
-    const unsigned mr_grid = 148 * 8;
+    p += cc * LIST_PER_CTA * 4;
+    uint32_t* ctr = reinterpret_cast<uint32_t*>(p);  // sieve survivors, base-2(p) passers
+    const unsigned mr_grid = 148 * (16 / SPRP_ILP);
     // CTAs [0, small_ctas) hold a special candidate or one below 10201
     uint64_t small_ctas = 0;
     while (small_ctas < ctas) {
@@ -411,7 +675,7 @@ extern "C" int rsa_safe_prime_scan(uint64_t lo, uint64_t hi, uint32_t* out, uint
     int rc;
     for (uint64_t c0 = 0; c0 < ctas; c0 += cc) {
         const uint64_t n = ctas - c0 < cc ? ctas - c0 : cc;
-        cudaError_t err = cudaMemsetAsync(ctr, 0, 3 * sizeof(uint32_t), st);
+        cudaError_t err = cudaMemsetAsync(ctr, 0, 2 * sizeof(uint32_t), st);
         if (err != cudaSuccess) { set_last_error("rsa_safe_prime_scan(memset)", err); return RSA_ECUDA; }
         // leading CTAs holding candidates below 10201 (or 5, 7) take the trial-division kernel
         const uint64_t nsmall = c0 < small_ctas ? (small_ctas - c0 < n ? small_ctas - c0 : n) : 0;
@@ -423,18 +687,17 @@ extern "C" int rsa_safe_prime_scan(uint64_t lo, uint64_t hi, uint32_t* out, uint
             k_scan_sieve<true><<<(unsigned)(n - nsmall), SCAN_BLOCK, 0, st>>>(R, c0 + nsmall, words, surv, ctr);
             if ((rc = launch_status("rsa_safe_prime_scan(sieve)"))) return rc;
         }
-        k_scan_sprp2<0><<<mr_grid, SCAN_BLOCK, 0, st>>>(R, surv, ctr, surv2, ctr + 1);
+        k_scan_sprp2<<<mr_grid, SCAN_BLOCK, 0, st>>>(R, surv, ctr, surv2, ctr + 1);
         if ((rc = launch_status("rsa_safe_prime_scan(sprp2 p)"))) return rc;
-        k_scan_sprp2<1><<<mr_grid, SCAN_BLOCK, 0, st>>>(R, surv2, ctr + 1, surv, ctr + 2);
-        if ((rc = launch_status("rsa_safe_prime_scan(sprp2 q)"))) return rc;
-        k_scan_mr761<<<mr_grid, SCAN_BLOCK, 0, st>>>(R, surv, ctr + 2, words);
-        if ((rc = launch_status("rsa_safe_prime_scan(mr 7,61)"))) return rc;
+        k_scan_final<<<mr_grid, SCAN_BLOCK, 0, st>>>(R, surv2, ctr + 1, words);
+        if ((rc = launch_status("rsa_safe_prime_scan(sprp2 q + table)"))) return rc;
     }
-    k_scan_counts<<<(unsigned)ctas, WORDS_PER_CTA, 0, st>>>(words, counts);
+    const unsigned tail_grid = (unsigned)(ctas < 148 * 16 ? ctas : 148 * 16);
+    k_scan_counts<<<tail_grid, TAIL_BLOCK, 0, st>>>(words, ctas, counts);
     if ((rc = launch_status("rsa_safe_prime_scan(counts)"))) return rc;
     k_scan_offsets<<<1, 1024, 0, st>>>(counts, ctas, offsets, count);
     if ((rc = launch_status("rsa_safe_prime_scan(offsets)"))) return rc;
-    k_scan_write<<<(unsigned)ctas, WORDS_PER_CTA, 0, st>>>(R, words, offsets, out, out_cap);
+    k_scan_write<<<tail_grid, TAIL_BLOCK, 0, st>>>(R, words, ctas, offsets, out, out_cap);
     return launch_status("rsa_safe_prime_scan(write)");
 }
 

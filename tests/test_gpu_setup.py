@@ -34,6 +34,27 @@ def test_scan_windows(lo, hi):
     assert got == want
 
 
+def test_scan_pseudoprime_neighbourhoods():
+    """Every candidate whose verdict the base-2 pseudoprime table decides (p or
+    (p-1)/2 is a base-2 strong pseudoprime and the other half passes base 2)
+    is scanned in a small window and compared with the C oracle."""
+    from test_spsp2_table import load_table, sprp2
+    _, _, vals = load_table()
+    decided = []
+    for t in vals:
+        if t % 12 == 11 and sprp2((t - 1) // 2):
+            decided.append(t)
+        if t % 6 == 5 and 2 * t + 1 < 1 << 32 and sprp2(2 * t + 1):
+            decided.append(2 * t + 1)
+    assert len(decided) == 55
+    for p in decided:
+        lo, hi = max(11, p - 600), min(1 << 32, p + 600)
+        got = R.safe_primes_in(lo, hi).cpu().numpy().tolist()
+        want, _ = coracle.census(lo, hi)
+        assert got == want.tolist(), p
+        assert p not in got
+
+
 def test_segment_stitching():
     a = R.safe_primes_in(2_000_000, 2_500_000).cpu().numpy()
     b = R.safe_primes_in(2_500_000, 3_000_000).cpu().numpy()
