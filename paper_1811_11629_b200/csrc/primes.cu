@@ -258,6 +258,49 @@ constexpr uint32_t SCAN_CHUNK_CTAS = RSA_SCAN_CHUNK_CTAS;
 constexpr uint64_t LIST_PER_CTA = SCAN_PER_CTA * 3 / 8;
 static_assert(4 * 1485 <= LIST_PER_CTA && SCAN_PER_CTA <= 4 * 5005, "survivor bound");
 
+// Wheel for 5, 7, 11, 13.  With s = -P0 12^-1 (mod 5005), candidate u of a
+// CTA has l | p_u iff u = s (mod l) and l | q_u iff u = s + 12^-1 (mod l), so
+// the CTA's sieve starts as the 5005-periodic byte pattern
+//   W[v] = [v = 0 or v = 12^-1 (mod l) for some l in {5, 7, 11, 13}]
+// read from offset t0 = -s = P0 12^-1 (mod 5005): one funnel-shifted copy
+// instead of ~16k byte marks per CTA.
+constexpr uint32_t WHEEL = 5 * 7 * 11 * 13;
+constexpr uint32_t cx_inv_mod(uint32_t a, uint32_t m) {
+    for (uint32_t x = 1; x < m; ++x)
+        if (a * x % m == 1) return x;
+    return 0;
+}
+constexpr uint32_t WHEEL_INV12 = cx_inv_mod(12, WHEEL);
+constexpr int WHEEL_WORDS = (int)((WHEEL + SCAN_PER_CTA + 3) / 4 + 1);
+struct Wheel {
+    uint32_t w[WHEEL_WORDS];
+};
+constexpr Wheel cx_wheel() {
+    Wheel t{};
+    const uint32_t ls[4] = {5, 7, 11, 13};
+    for (uint32_t x = 0; x < 4u * WHEEL_WORDS; ++x) {
+        const uint32_t v = x % WHEEL;
+        bool m = false;
+        for (uint32_t l : ls) m = m || v % l == 0 || v % l == WHEEL_INV12 % l;
+        if (m) t.w[x / 4] |= 1u << (8 * (x % 4));
+    }
+    return t;
+}
+__device__ const Wheel g_wheel = cx_wheel();
+
+// first u with l | p_u (q = false) or l | q_u (q = true), inv = 12^-1 or 6^-1 mod l
+RSA_DEV uint32_t sieve_start(uint64_t P0, uint32_t l, uint32_t inv, bool q) {
+    const uint64_t v = q ? (P0 - 1) >> 1 : P0;
+    const uint32_t r = ((uint32_t)(v >> 32) * ((0u - l) % l) + (uint32_t)v % l) % l;
+    return (l - r) % l * inv % l;
+}
+
+// sieve tiers over c_sieve: [0, 4) the wheel, [4, 16) CTA-cooperative marking,
+// [16, NSIEVE) warp-cooperative, then g_big one entry per thread
+constexpr int TIER_A0 = 4, TIER_B0 = 16;
+static_assert(2 * (TIER_B0 - TIER_A0) <= SCAN_BLOCK, "tier-A starts: one thread each");
+static_assert(2 * (NSIEVE - TIER_B0) <= 32 * (SCAN_BLOCK / 32), "tier-B entries: <= 32 per warp");
+
 // SIEVE = true: CTAs whose candidates are all 11 mod 12 and >= 10201 (no
 // sieving prime divides p or q trivially, MR's bases are below n);
 // SIEVE = false: the (at most one or two) leading CTAs of a range that starts
@@ -269,7 +312,7 @@ k_scan_sieve(ScanRange R, uint64_t cta0, uint32_t* __restrict__ words, uint32_t*
              uint32_t* __restrict__ nsurv) {
     __shared__ uint32_t flags[SIEVE ? 1 : WORDS_PER_CTA];
     __shared__ __align__(16) uint8_t comp[SIEVE ? SCAN_PER_CTA : 4];
-    __shared__ uint16_t start[2 * NSIEVE];
+    __shared__ uint16_t start[SIEVE ? 2 * (TIER_B0 - TIER_A0) : 1];
     __shared__ uint16_t wcnt[SIEVE ? 1 : SCAN_ITERS][SCAN_BLOCK / 32];  // survivors per (iteration, warp)
     __shared__ uint32_t gbase;
     const uint64_t cta = cta0 + blockIdx.x;
@@ -278,24 +321,43 @@ k_scan_sieve(ScanRange R, uint64_t cta0, uint32_t* __restrict__ words, uint32_t*
     if constexpr (!SIEVE)
         for (uint32_t w = threadIdx.x; w < WORDS_PER_CTA; w += SCAN_BLOCK) flags[w] = 0;
     if constexpr (SIEVE) {
-        uint4* c4z = reinterpret_cast<uint4*>(comp);
-        for (uint32_t u = threadIdx.x; u < SCAN_PER_CTA / 16; u += SCAN_BLOCK) c4z[u] = make_uint4(0, 0, 0, 0);
-        if (threadIdx.x < 2 * NSIEVE) {
-            const SievePrime sp = c_sieve[threadIdx.x >> 1];
-            const uint64_t P0 = R.first + 12ull * (base - R.nspec);
-            const uint32_t l = sp.l;
-            uint32_t r, inv;
-            if (threadIdx.x & 1) { r = (uint32_t)(((P0 - 1) >> 1) % l); inv = sp.inv6; }
-            else { r = (uint32_t)(P0 % l); inv = sp.inv12; }
-            start[threadIdx.x] = (uint16_t)(((l - r) % l) * inv % l);
+        const uint64_t P0 = R.first + 12ull * (base - R.nspec);
+        {   // wheel copy (5, 7, 11, 13)
+            const uint32_t t0 = (uint32_t)(P0 % WHEEL) * WHEEL_INV12 % WHEEL;
+            const uint32_t a0 = t0 >> 2, sh = (t0 & 3) * 8;
+            uint32_t* c32 = reinterpret_cast<uint32_t*>(comp);
+            for (uint32_t x = threadIdx.x; x < SCAN_PER_CTA / 4; x += SCAN_BLOCK)
+                c32[x] = __funnelshift_r(__ldg(&g_wheel.w[a0 + x]), __ldg(&g_wheel.w[a0 + x + 1]), sh);
         }
-        __syncthreads();
-        for (int k = 0; k < 2 * NSIEVE; ++k) {
-            const uint32_t l = c_sieve[k >> 1].l;
+        if (threadIdx.x < 2 * (TIER_B0 - TIER_A0)) {
+            const uint32_t k = 2 * TIER_A0 + threadIdx.x;
+            const SievePrime sp = c_sieve[k >> 1];
+            start[threadIdx.x] = (uint16_t)sieve_start(P0, sp.l, (k & 1) ? sp.inv6 : sp.inv12, k & 1);
+        }
+        __syncthreads();  // wheel stored, tier-A starts ready
+        // tier A: primes 17..61, the whole CTA strides through each entry
+        for (int k = 0; k < 2 * (TIER_B0 - TIER_A0); ++k) {
+            const uint32_t l = c_sieve[TIER_A0 + (k >> 1)].l;
             for (uint32_t u = start[k] + l * threadIdx.x; u < SCAN_PER_CTA; u += l * SCAN_BLOCK) comp[u] = 1;
         }
-        {   // large primes: one (prime, p-or-q) entry per thread at a time
-            const uint64_t P0 = R.first + 12ull * (base - R.nspec), Q0 = (P0 - 1) >> 1;
+        {   // tier B: primes 67..251, entries dealt to warps, lanes stride each entry
+            constexpr int NB_ENT = 2 * (NSIEVE - TIER_B0);
+            constexpr int NWARP = SCAN_BLOCK / 32;
+            const int e_l = warp + NWARP * lane;  // entry whose start this lane computes
+            uint32_t st = 0;
+            if (e_l < NB_ENT) {
+                const uint32_t k = 2 * TIER_B0 + e_l;
+                const SievePrime sp = c_sieve[k >> 1];
+                st = sieve_start(P0, sp.l, (k & 1) ? sp.inv6 : sp.inv12, k & 1);
+            }
+            for (int i = 0; warp + NWARP * i < NB_ENT; ++i) {
+                const uint32_t s0 = __shfl_sync(0xffffffffu, st, i);
+                const uint32_t l = c_sieve[TIER_B0 + ((warp + NWARP * i) >> 1)].l;
+                for (uint32_t u = s0 + l * lane; u < SCAN_PER_CTA; u += 32 * l) comp[u] = 1;
+            }
+        }
+        {   // tier C: primes 257..RSA_SIEVE_MAX, one (prime, p-or-q) entry per thread at a time
+            const uint64_t Q0 = (P0 - 1) >> 1;
             for (uint32_t k = threadIdx.x; k < 2u * NBIG; k += SCAN_BLOCK) {
                 const BigPrime bp = g_big.e[k >> 1];
                 const uint32_t l = bp.l;
