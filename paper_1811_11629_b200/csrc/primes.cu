@@ -88,6 +88,7 @@ constexpr int cx_count_primes(uint32_t lo, uint32_t hi) {
 constexpr int NBIG = cx_count_primes(257, RSA_SIEVE_MAX);
 struct BigPrime {
     uint16_t l, inv12, inv6, r32;  // r32 = 2^32 mod l
+    uint64_t M;                    // floor((2^64 - 1) / l) + 1: a mod l = mulhi64(M a, l) for 32-bit a
 };
 struct BigTable {
     BigPrime e[NBIG];
@@ -98,7 +99,7 @@ constexpr BigTable cx_big_table() {
     for (uint32_t n = 257; n < RSA_SIEVE_MAX; ++n)
         if (cx_is_prime(n))
             t.e[k++] = BigPrime{(uint16_t)n, (uint16_t)cx_powmod(12, n - 2, n), (uint16_t)cx_powmod(6, n - 2, n),
-                                (uint16_t)((1ull << 32) % n)};
+                                (uint16_t)((1ull << 32) % n), ~0ull / n + 1};
     return t;
 }
 static_assert(RSA_SIEVE_MAX <= 65536 && RSA_SIEVE_MAX < 10201, "sieve primes must stay below the smallest sieved candidate");
@@ -362,9 +363,12 @@ k_scan_sieve(ScanRange R, uint64_t cta0, uint32_t* __restrict__ words, uint32_t*
                 const BigPrime bp = g_big.e[k >> 1];
                 const uint32_t l = bp.l;
                 const uint64_t v = (k & 1) ? Q0 : P0;
-                const uint32_t r = ((uint32_t)(v >> 32) * bp.r32 + (uint32_t)v % l) % l;
+                // Lemire's fastmod (a mod l = mulhi64(M a, l)) instead of two 32-bit divisions
+                uint32_t r = (uint32_t)__umul64hi(bp.M * (uint32_t)v, l) + (uint32_t)(v >> 32) * bp.r32;
+                r = r >= l ? r - l : r;
                 const uint32_t inv = (k & 1) ? bp.inv6 : bp.inv12;
-                for (uint32_t u = (l - r) % l * inv % l; u < SCAN_PER_CTA; u += l) comp[u] = 1;
+                const uint32_t neg = r ? l - r : 0;
+                for (uint32_t u = (uint32_t)__umul64hi(bp.M * (neg * inv), l); u < SCAN_PER_CTA; u += l) comp[u] = 1;
             }
         }
     }
