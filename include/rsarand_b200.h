@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define RSA_ABI_VERSION 1
+#define RSA_ABI_VERSION 2
 
 /* status codes */
 #define RSA_OK 0
@@ -173,13 +173,21 @@ int rsa_safe_prime_scan(uint64_t lo, uint64_t hi, uint32_t* out, uint64_t out_ca
 int rsa_is_safe_prime32(const uint32_t* n, uint64_t count, uint8_t* is_prime,
                         uint8_t* is_safe, void* stream);
 
+/* Bucket index of a sorted u32 table: index[b] = number of entries < b*2^16,
+ * b = 0..65536 (RSA_SP_INDEX_LEN entries).  Lets rsa_find_pair /
+ * rsa_setup_instances start their search inside one 2^16-wide bucket
+ * (~90 safe primes) instead of the whole table. */
+#define RSA_SP_INDEX_LEN 65537u
+int rsa_safe_prime_index(const uint32_t* sp, uint64_t n_sp, uint32_t* index, void* stream);
+
 /* find_pair (paramfactory.py:195-219) for a batch of p1 values against the
  * sorted safe-prime table sp[0..n_sp): p2 = nearest table entry to floor(q/p1),
  * ties to the smaller, p2 != p1, 2^31 < p2 < 2^32, |p1*p2 - q| <= tol.
+ * sp_index = rsa_safe_prime_index of sp, or NULL (plain binary search).
  * status[j] = 0 found, 1 NotFound. */
 int rsa_find_pair(const uint32_t* p1, uint64_t count, uint64_t q, uint64_t tol,
-                  const uint32_t* sp, uint64_t n_sp, uint32_t* p2, int32_t* status,
-                  void* stream);
+                  const uint32_t* sp, uint64_t n_sp, const uint32_t* sp_index,
+                  uint32_t* p2, int32_t* status, void* stream);
 
 /* ---------------------------------------------------------------------------
  * K4: instance setup.  Replaces paramfactory.derive_stream_params +
@@ -189,7 +197,8 @@ int rsa_find_pair(const uint32_t* p1, uint64_t count, uint64_t q, uint64_t tol,
  *   ordinal = beta mod K_P1, a = mult[beta/(K_P1*K_P2) mod n_a] (or `multiplier`)
  *   p1 = p1tab[(ordinal+step) mod K_P1], step = 0..255, first with a find_pair partner.
  * seed_mod_S = master_seed mod S (reduced by the caller, exact for any seed size).
- * sp = sorted safe primes of [2^31, 2^32); p1tab = its prefix inside the p1 window.
+ * sp = sorted safe primes of [2^31, 2^32) (sp_index: its rsa_safe_prime_index, or
+ * NULL); p1tab = its prefix inside the p1 window.
  * Steps start at cfg->start_step (0 for the reference order; a host caller
  * that rejects a pair for a host-only reason resumes after it).
  * status[j] = 0 ok, 2 DerivationExhausted; step_out[j] = ordinal advance (may be NULL).
@@ -211,7 +220,7 @@ typedef struct rsa_setup_config {
 
 int rsa_setup_instances(const rsa_setup_config* cfg, uint64_t count,
                         const uint32_t* mult_table, const uint32_t* sp, uint64_t n_sp,
-                        const uint32_t* p1tab, uint64_t n_p1tab,
+                        const uint32_t* sp_index, const uint32_t* p1tab, uint64_t n_p1tab,
                         rsa_instance* out, int32_t* status, uint32_t* step_out,
                         void* stream);
 

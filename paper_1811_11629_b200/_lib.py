@@ -53,6 +53,8 @@ class SetupConfig(ctypes.Structure):
                 ("max_steps", c_u32), ("start_step", c_u32)]
 
 
+ABI_VERSION = 2  # include/rsarand_b200.h RSA_ABI_VERSION
+
 # name -> (restype, argtypes); the CPU test checks this list against include/*.h
 PROTOTYPES = {
     "rsa_fill": (ctypes.c_int, [c_vp, c_u32, c_u32, c_u64, c_u32, c_u32, c_vp, c_vp, c_vp,
@@ -70,9 +72,10 @@ PROTOTYPES = {
     "rsa_safe_prime_scan_scratch_bytes": (c_u64, [c_u64, c_u64]),
     "rsa_safe_prime_scan": (ctypes.c_int, [c_u64, c_u64, c_vp, c_u64, c_vp, c_vp, c_u64, c_vp]),
     "rsa_is_safe_prime32": (ctypes.c_int, [c_vp, c_u64, c_vp, c_vp, c_vp]),
-    "rsa_find_pair": (ctypes.c_int, [c_vp, c_u64, c_u64, c_u64, c_vp, c_u64, c_vp, c_vp, c_vp]),
+    "rsa_safe_prime_index": (ctypes.c_int, [c_vp, c_u64, c_vp, c_vp]),
+    "rsa_find_pair": (ctypes.c_int, [c_vp, c_u64, c_u64, c_u64, c_vp, c_u64, c_vp, c_vp, c_vp, c_vp]),
     "rsa_setup_instances": (ctypes.c_int, [ctypes.POINTER(SetupConfig), c_u64, c_vp, c_vp, c_u64,
-                                           c_vp, c_u64, c_vp, c_vp, c_vp, c_vp]),
+                                           c_vp, c_vp, c_u64, c_vp, c_vp, c_vp, c_vp]),
     "rsa_probe_imad": (ctypes.c_int, [c_u32, c_u32, c_vp, ctypes.POINTER(ctypes.c_double), c_vp]),
     "rsa_battery_count": (ctypes.c_int, [ctypes.c_int, c_vp, c_u64, c_u32, c_u32, c_vp, c_vp, c_vp]),
     "rsa_abi_version": (ctypes.c_int, []),
@@ -108,7 +111,7 @@ def load(build_if_missing: bool = True):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.rsa_abi_version() != 1:
+        if lib.rsa_abi_version() != ABI_VERSION:
             raise RsaCudaError("librsarand_b200 ABI mismatch")
         _LIB = lib
         return lib

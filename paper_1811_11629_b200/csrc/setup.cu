@@ -22,11 +22,21 @@ RSA_DEV bool pair_ok(uint32_t p1, uint32_t c, uint64_t q, uint64_t tol) {
     return d <= tol;
 }
 
-// 0 = found (*p2 set), 1 = NotFound.
+// 0 = found (*p2 set), 1 = NotFound.  idx (optional): rsa_safe_prime_index of
+// sp, narrowing the search to the 2^16-wide bucket of the target.
 RSA_DEV int find_partner(uint32_t p1, uint64_t q, uint64_t tol, const uint32_t* __restrict__ sp,
-                         uint64_t n_sp, uint32_t* p2) {
+                         uint64_t n_sp, const uint32_t* __restrict__ idx, uint32_t* p2) {
     uint64_t target = q / p1;
     uint64_t lo = 0, hi = n_sp;  // first index with sp[idx] > target
+    if (idx) {
+        if (target >= 0xFFFFFFFFull) {
+            lo = hi = n_sp;
+        } else {  // entries with value >> 16 == b lie in [idx[b], idx[b+1])
+            const uint32_t b = (uint32_t)(target >> 16);
+            lo = __ldg(idx + b);
+            hi = __ldg(idx + b + 1);
+        }
+    }
     while (lo < hi) {
         uint64_t mid = (lo + hi) >> 1;
         if ((uint64_t)__ldg(sp + mid) <= target) lo = mid + 1;
@@ -79,8 +89,42 @@ RSA_DEV void build_instance(rsa_instance* o, uint32_t p1, uint32_t p2, uint32_t 
     *o = v;
 }
 
+// x*y mod m for x, y < m < 2^50: the quotient from an FP64 estimate is off by
+// at most one (relative error <= 3 * 2^-53 on a quotient < 2^50), and the
+// remainder is formed exactly in wrapping 64-bit arithmetic.
+RSA_DEV uint64_t mulmod50(uint64_t x, uint64_t y, uint64_t m, double minv) {
+    const uint64_t qd = (uint64_t)(__dmul_rn(__dmul_rn((double)x, (double)y), minv));
+    int64_t r = (int64_t)(x * y - qd * m);
+    if (r < 0) r += (int64_t)m;
+    else if (r >= (int64_t)m) r -= (int64_t)m;
+    return (uint64_t)r;
+}
+
+RSA_DEV uint64_t powmod50(uint64_t b, uint32_t e, uint64_t m, double minv) {
+    uint64_t r = 1;
+    while (e) {
+        if (e & 1) r = mulmod50(r, b, m, minv);
+        e >>= 1;
+        if (e) b = mulmod50(b, b, m, minv);
+    }
+    return r;
+}
+
+__global__ void k_sp_index(const uint32_t* __restrict__ sp, uint64_t n_sp, uint32_t* __restrict__ index) {
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= RSA_SP_INDEX_LEN) return;
+    const uint64_t key = (uint64_t)b << 16;  // lower_bound(key)
+    uint64_t lo = 0, hi = n_sp;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if ((uint64_t)sp[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    index[b] = (uint32_t)lo;
+}
+
 __global__ void k_setup(rsa_setup_config cfg, uint64_t count, const uint32_t* __restrict__ mult,
-                        const uint32_t* __restrict__ sp, uint64_t n_sp,
+                        const uint32_t* __restrict__ sp, uint64_t n_sp, const uint32_t* __restrict__ sp_index,
                         const uint32_t* __restrict__ p1tab, uint64_t n_p1tab,
                         rsa_instance* __restrict__ out, int32_t* __restrict__ status,
                         uint32_t* __restrict__ step_out) {
@@ -88,9 +132,19 @@ __global__ void k_setup(rsa_setup_config cfg, uint64_t count, const uint32_t* __
     if (j >= count) return;
     // beta = (t + id*SIGMA mod S)^EPSILON mod S   (paramfactory.py:242-250)
     const uint64_t S = cfg.k_p1 * cfg.k_p2 * cfg.n_mult;
-    uint64_t id_mod = (uint64_t)(((unsigned __int128)cfg.first_id + j) % S);
-    uint64_t x = (uint64_t)(((unsigned __int128)cfg.seed_mod_S + mulmod64(id_mod, cfg.sigma % S, S)) % S);
-    uint64_t beta = powmod64(x, cfg.epsilon, S);
+    uint64_t beta;
+    if (S < (1ull << 50)) {  // the published radices: S = K_P1*K_P2*n_a ~ 2^45
+        const double Sinv = 1.0 / (double)S;
+        uint64_t id_mod = cfg.first_id % S + (j < S ? j : j % S);
+        id_mod = id_mod >= S ? id_mod - S : id_mod;
+        uint64_t x = cfg.seed_mod_S % S + mulmod50(id_mod, cfg.sigma % S, S, Sinv);
+        x = x >= S ? x - S : x;
+        beta = powmod50(x, cfg.epsilon, S, Sinv);
+    } else {
+        uint64_t id_mod = (uint64_t)(((unsigned __int128)cfg.first_id + j) % S);
+        uint64_t x = (uint64_t)(((unsigned __int128)cfg.seed_mod_S + mulmod64(id_mod, cfg.sigma % S, S)) % S);
+        beta = powmod64(x, cfg.epsilon, S);
+    }
     uint64_t ordinal = beta % cfg.k_p1;
     uint32_t a = cfg.multiplier ? cfg.multiplier : mult[(beta / (cfg.k_p1 * cfg.k_p2)) % cfg.n_mult];
     // bounded ordinal advance (paramfactory.py:270-278)
@@ -98,7 +152,7 @@ __global__ void k_setup(rsa_setup_config cfg, uint64_t count, const uint32_t* __
         uint64_t k = (ordinal + step) % cfg.k_p1;
         if (k >= n_p1tab) break;
         uint32_t p1 = __ldg(p1tab + k), p2;
-        if (find_partner(p1, cfg.q, cfg.tol, sp, n_sp, &p2) == 0) {
+        if (find_partner(p1, cfg.q, cfg.tol, sp, n_sp, sp_index, &p2) == 0) {
             build_instance(out + j, p1, p2, a, cfg.e, cfg.q);
             status[j] = 0;
             if (step_out) step_out[j] = step;
@@ -110,12 +164,12 @@ __global__ void k_setup(rsa_setup_config cfg, uint64_t count, const uint32_t* __
 }
 
 __global__ void k_find_pair(const uint32_t* __restrict__ p1, uint64_t count, uint64_t q, uint64_t tol,
-                            const uint32_t* __restrict__ sp, uint64_t n_sp, uint32_t* __restrict__ p2,
-                            int32_t* __restrict__ status) {
+                            const uint32_t* __restrict__ sp, uint64_t n_sp, const uint32_t* __restrict__ sp_index,
+                            uint32_t* __restrict__ p2, int32_t* __restrict__ status) {
     uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= count) return;
     uint32_t v = 0;
-    status[j] = find_partner(p1[j], q, tol, sp, n_sp, &v);
+    status[j] = find_partner(p1[j], q, tol, sp, n_sp, sp_index, &v);
     p2[j] = v;
 }
 
@@ -123,24 +177,30 @@ __global__ void k_find_pair(const uint32_t* __restrict__ p1, uint64_t count, uin
 
 using namespace rsa;
 
+extern "C" int rsa_safe_prime_index(const uint32_t* sp, uint64_t n_sp, uint32_t* index, void* stream) {
+    if ((!sp && n_sp) || !index || n_sp >= (1ull << 32)) return RSA_EINVAL;
+    k_sp_index<<<grid_for(RSA_SP_INDEX_LEN, 256), 256, 0, as_stream(stream)>>>(sp, n_sp, index);
+    return launch_status("rsa_safe_prime_index");
+}
+
 extern "C" int rsa_setup_instances(const rsa_setup_config* cfg, uint64_t count,
                                    const uint32_t* mult_table, const uint32_t* sp, uint64_t n_sp,
-                                   const uint32_t* p1tab, uint64_t n_p1tab, rsa_instance* out,
-                                   int32_t* status, uint32_t* step_out, void* stream) {
+                                   const uint32_t* sp_index, const uint32_t* p1tab, uint64_t n_p1tab,
+                                   rsa_instance* out, int32_t* status, uint32_t* step_out, void* stream) {
     if (!cfg || !sp || !p1tab || !out || !status || count == 0) return RSA_EINVAL;
     if (cfg->k_p1 == 0 || cfg->k_p2 == 0 || cfg->n_mult == 0 || cfg->e == 0 || cfg->q < 3) return RSA_EINVAL;
     if (!cfg->multiplier && !mult_table) return RSA_EINVAL;
-    k_setup<<<grid_for(count, 128), 128, 0, as_stream(stream)>>>(*cfg, count, mult_table, sp, n_sp, p1tab,
-                                                                n_p1tab, out, status, step_out);
+    k_setup<<<grid_for(count, 128), 128, 0, as_stream(stream)>>>(*cfg, count, mult_table, sp, n_sp, sp_index,
+                                                                p1tab, n_p1tab, out, status, step_out);
     return launch_status("rsa_setup_instances");
 }
 
 extern "C" int rsa_find_pair(const uint32_t* p1, uint64_t count, uint64_t q, uint64_t tol,
-                             const uint32_t* sp, uint64_t n_sp, uint32_t* p2, int32_t* status,
-                             void* stream) {
+                             const uint32_t* sp, uint64_t n_sp, const uint32_t* sp_index, uint32_t* p2,
+                             int32_t* status, void* stream) {
     if (!p1 || !sp || !p2 || !status) return RSA_EINVAL;
     if (count == 0) return RSA_OK;
-    k_find_pair<<<grid_for(count, 128), 128, 0, as_stream(stream)>>>(p1, count, q, tol, sp, n_sp, p2,
-                                                                     status);
+    k_find_pair<<<grid_for(count, 128), 128, 0, as_stream(stream)>>>(p1, count, q, tol, sp, n_sp, sp_index,
+                                                                     p2, status);
     return launch_status("rsa_find_pair");
 }

@@ -107,6 +107,17 @@ def nth_safe_prime_in(lo: int, hi: int, k: int, dev=None) -> int:
     raise NotFound(f"fewer than {k + 1} safe primes in [{lo}, {hi})")
 
 
+def safe_prime_index(sp: torch.Tensor) -> torch.Tensor:
+    """Bucket index of a sorted device u32 table (rsa_safe_prime_index):
+    index[b] = number of entries below b*2^16, b = 0..65536."""
+    idx = torch.empty(SP_INDEX_LEN, dtype=torch.int32, device=sp.device)
+    _lib.call("rsa_safe_prime_index", sp.data_ptr(), int(sp.numel()), idx.data_ptr(), _device.stream(sp.device))
+    return idx
+
+
+SP_INDEX_LEN = 65537
+
+
 class SafePrimeTable:
     """All safe primes of [2^31, 2^32) on one device (the p1 table is its
     prefix inside P1_WINDOW)."""
@@ -117,6 +128,7 @@ class SafePrimeTable:
         self.n_sp = int(self.sp.numel())
         as64 = self.sp.to(torch.int64)
         self.n_p1 = int(torch.searchsorted(as64, torch.tensor([P1_WINDOW[1]], device=dev)).item())
+        self.index = safe_prime_index(self.sp)
         self.mult_cache: dict = {}
 
     def mult_table(self, table: tuple) -> torch.Tensor:
@@ -168,7 +180,7 @@ def find_pair(p1: int, q: int = Q_DEFAULT, tol: float = DEFAULT_TOLERANCE, dev=N
     p2 = torch.zeros(1, dtype=torch.uint32, device=d)
     st = torch.zeros(1, dtype=torch.int32, device=d)
     _lib.call("rsa_find_pair", p1t.data_ptr(), 1, q, min(t, (1 << 64) - 1), tab.sp.data_ptr(),
-              tab.n_sp, p2.data_ptr(), st.data_ptr(), _device.stream(d))
+              tab.n_sp, tab.index.data_ptr(), p2.data_ptr(), st.data_ptr(), _device.stream(d))
     if int(st.item()) != 0:
         raise NotFound(f"no safe-prime partner for p1={p1} within {tol} of q")
     return p1, int(p2.to(torch.int64).item())
@@ -269,7 +281,7 @@ def _run_setup(cfg: _lib.SetupConfig, count: int, table: tuple, dev) -> Instance
     steps = torch.empty(count, dtype=torch.int32, device=d)
     mult = tab.mult_table(table)
     _lib.call("rsa_setup_instances", cfg, count, mult.data_ptr(), tab.sp.data_ptr(), tab.n_sp,
-              tab.sp.data_ptr(), tab.n_p1, inst.data_ptr(), status.data_ptr(), steps.data_ptr(),
+              tab.index.data_ptr(), tab.sp.data_ptr(), tab.n_p1, inst.data_ptr(), status.data_ptr(), steps.data_ptr(),
               _device.stream(d))
     return InstanceTable(inst, status, steps, 0, cfg.first_id, cfg.e)
 
@@ -296,9 +308,8 @@ def derive_params_table(master_seed: int, first_id: int, count: int, e: int = rs
     cfg = _setup_config(master_seed, first_id, e, len(multiplier_table), multiplier or 0)
     t = _run_setup(cfg, count, tuple(multiplier_table), dev)
     t.master_seed = master_seed
-    bad = torch.nonzero(t.status != 0)
-    if bad.numel():
-        j = int(bad[0].item())
+    if int(torch.count_nonzero(t.status).item()):
+        j = int(torch.nonzero(t.status != 0)[0].item())
         raise DerivationExhausted(f"no valid parameters for stream id {first_id + j}")
     return t
 

@@ -152,3 +152,54 @@ def test_table_e_and_errors(golden_streams):
     assert (t.records()["e"] == 17).all()
     with pytest.raises(R.DerivationExhausted):
         R.derive_params_table(0, 0, 4, e=259)
+
+
+def test_safe_prime_index_and_unindexed_search(golden_streams):
+    """The bucket index matches searchsorted, and the indexed search returns
+    byte-identical instances / pairs to the plain binary search (NULL index)."""
+    tab = paramfactory.safe_prime_table()
+    keys = torch.arange(paramfactory.SP_INDEX_LEN, dtype=torch.int64, device=tab.sp.device) << 16
+    want = torch.searchsorted(tab.sp.to(torch.int64), keys)
+    assert torch.equal(tab.index.to(torch.int64), want)
+    n = 1 << 16
+    cfg = paramfactory._setup_config(golden_streams["master_seed"], 12345, 9,
+                                     len(paramfactory.MULTIPLIER_TABLE), 0)
+    mult = tab.mult_table(tuple(paramfactory.MULTIPLIER_TABLE))
+    outs = []
+    for idx in (tab.index.data_ptr(), None):
+        inst = torch.empty((n, 128), dtype=torch.uint8, device=tab.sp.device)
+        st = torch.empty(n, dtype=torch.int32, device=tab.sp.device)
+        steps = torch.empty(n, dtype=torch.int32, device=tab.sp.device)
+        _lib.call("rsa_setup_instances", cfg, n, mult.data_ptr(), tab.sp.data_ptr(), tab.n_sp, idx,
+                  tab.sp.data_ptr(), tab.n_p1, inst.data_ptr(), st.data_ptr(), steps.data_ptr(), None)
+        outs.append((inst.cpu(), st.cpu(), steps.cpu()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    p1 = tab.sp[:: max(1, tab.n_p1 // 4096)][:4096].contiguous()
+    res = []
+    for idx in (tab.index.data_ptr(), None):
+        p2 = torch.zeros(p1.numel(), dtype=torch.int32, device=p1.device)
+        st = torch.zeros(p1.numel(), dtype=torch.int32, device=p1.device)
+        _lib.call("rsa_find_pair", p1.data_ptr(), p1.numel(), paramfactory.Q_DEFAULT,
+                  paramfactory.tolerance_int(paramfactory.DEFAULT_TOLERANCE, paramfactory.Q_DEFAULT),
+                  tab.sp.data_ptr(), tab.n_sp, idx, p2.data_ptr(), st.data_ptr(), None)
+        res.append((p2.cpu(), st.cpu()))
+    assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
+    assert (res[0][1] == 0).sum() > 0
+
+
+@pytest.mark.parametrize("n_a", [len(paramfactory.MULTIPLIER_TABLE), 494])
+def test_stream_indices_both_index_space_paths(n_a, golden_streams):
+    """S = K_P1*K_P2*n_a below 2^50 takes the FP64-quotient mulmod, above it
+    the 128-bit path; both must reproduce the host's exact stream_indices."""
+    table = tuple(paramfactory.MULTIPLIER_TABLE[i % len(paramfactory.MULTIPLIER_TABLE)] for i in range(n_a))
+    assert (paramfactory._index_space(n_a) >= 1 << 50) == (n_a == 494)
+    seed, first, n = golden_streams["master_seed"], (1 << 40) + 7, 512
+    t = R.derive_params_table(seed, first, n, multiplier_table=table)
+    rec = t.records()
+    steps = t.steps.cpu().numpy()
+    sp = paramfactory.safe_prime_table().sp.cpu().numpy().view(np.uint32)
+    for j in range(n):
+        ordinal, ai = paramfactory.stream_indices(paramfactory.StreamKey(seed, first + j), n_a)
+        assert int(rec[j]["a"]) == table[ai]
+        assert int(rec[j]["p1"]) == int(sp[(ordinal + int(steps[j])) % paramfactory.K_P1])
