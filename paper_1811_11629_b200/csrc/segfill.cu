@@ -70,6 +70,60 @@ k_seg_sums(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t lanes, u
     sums[2 * t + 1] = a2;
 }
 
+// Exclusive scan over the segments of each lane (in place), mod p1 / p2:
+// one CTA per lane, each thread reduces a run of consecutive segments, a
+// block scan (warp shuffles + one smem pass) combines the runs, and each
+// thread rewrites its run with the running prefix.  Modular addition is
+// associative, so the result equals the sequential scan.
+__global__ void __launch_bounds__(1024)
+k_seg_scan_block(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t lanes, uint64_t nseg,
+                 uint32_t* __restrict__ sums) {
+    __shared__ uint32_t w1[32], w2[32];
+    const uint64_t lane = blockIdx.x;
+    const rsa_instance* ip = inst + lane / mv;
+    const uint32_t p1 = ip->p1, p2 = ip->p2;
+    const uint64_t per = (nseg + blockDim.x - 1) / blockDim.x;
+    const uint64_t j0 = threadIdx.x * per, j1 = min(nseg, j0 + per);
+    uint32_t a1 = 0, a2 = 0;
+    for (uint64_t j = j0; j < j1; ++j) {
+        const uint64_t t = j * lanes + lane;
+        a1 = add_mod(a1, sums[2 * t], p1);
+        a2 = add_mod(a2, sums[2 * t + 1], p2);
+    }
+    // inclusive scan of (a1, a2) over the threads
+    const int wl = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    uint32_t i1 = a1, i2 = a2;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o1 = __shfl_up_sync(0xffffffffu, i1, d), o2 = __shfl_up_sync(0xffffffffu, i2, d);
+        if (wl >= d) { i1 = add_mod(i1, o1, p1); i2 = add_mod(i2, o2, p2); }
+    }
+    if (wl == 31) { w1[wid] = i1; w2[wid] = i2; }
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t x1 = wl < nw ? w1[wl] : 0, x2 = wl < nw ? w2[wl] : 0;
+        uint32_t y1 = x1, y2 = x2;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o1 = __shfl_up_sync(0xffffffffu, y1, d), o2 = __shfl_up_sync(0xffffffffu, y2, d);
+            if (wl >= d) { y1 = add_mod(y1, o1, p1); y2 = add_mod(y2, o2, p2); }
+        }
+        if (wl < nw) { w1[wl] = sub_mod(y1, x1, p1); w2[wl] = sub_mod(y2, x2, p2); }  // exclusive
+    }
+    __syncthreads();
+    // exclusive prefix of this thread's run
+    uint32_t r1 = add_mod(w1[wid], sub_mod(i1, a1, p1), p1);
+    uint32_t r2 = add_mod(w2[wid], sub_mod(i2, a2, p2), p2);
+    for (uint64_t j = j0; j < j1; ++j) {
+        const uint64_t t = j * lanes + lane;
+        const uint32_t v1 = sums[2 * t], v2 = sums[2 * t + 1];
+        sums[2 * t] = r1;
+        sums[2 * t + 1] = r2;
+        r1 = add_mod(r1, v1, p1);
+        r2 = add_mod(r2, v2, p2);
+    }
+}
+
 // exclusive scan over the segments of each lane (in place), mod p1 / p2
 __global__ void k_seg_scan(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t lanes,
                            uint64_t nseg, uint32_t* __restrict__ sums) {
@@ -171,7 +225,13 @@ extern "C" int rsa_fill_segmented(const rsa_instance* inst, uint32_t n_inst, uin
     k_seg_sums<<<grid_for(threads, 256), 256, 0, st>>>(inst, mv, lanes, blocks, L, nseg_eff, m1, m2, s, st0, sums);
     int rc = launch_status("rsa_fill_segmented(sums)");
     if (rc) return rc;
-    k_seg_scan<<<grid_for(lanes, 128), 128, 0, st>>>(inst, mv, lanes, nseg_eff, sums);
+    if (nseg_eff >= 64) {  // long segment chains: one CTA per lane
+        unsigned tb = 32;
+        while (tb < 1024 && tb * 8 < nseg_eff) tb <<= 1;
+        k_seg_scan_block<<<(unsigned)lanes, tb, 0, st>>>(inst, mv, lanes, nseg_eff, sums);
+    } else {
+        k_seg_scan<<<grid_for(lanes, 128), 128, 0, st>>>(inst, mv, lanes, nseg_eff, sums);
+    }
     if ((rc = launch_status("rsa_fill_segmented(scan)"))) return rc;
     const unsigned grid = grid_for(threads, 256);
     switch (e) {
