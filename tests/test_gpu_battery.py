@@ -69,3 +69,22 @@ def test_poker_and_collision_tables():
     assert abs(stats.poker_probabilities().sum() - 1.0) < 1e-15
     d = stats.collision_distribution(4, 8)
     assert abs(d.sum() - 1.0) < 1e-12
+
+
+def test_weakened_modes():
+    """Reference acceptance c11 (test_acceptance.py:234-253): the unit skip with
+    e=9 passes the battery at budget 1e7; the identity cipher (e=1, test mode)
+    on a counter fails frequency / serial_d2 / max_of_t."""
+    from paper_1811_11629_b200 import rsacore
+    p = R.derive_stream_params(R.StreamKey(R.DEFAULT_MASTER_SEED, 0))
+
+    def factory(params):
+        return lambda sel: bitsource.BitSource([R.init_vector(params, m0=0, s0=1, mv=65536)], sel)
+
+    unit9 = rsacore.make_params(p.p1, p.p2, 9, p.skip, skip_mode=rsacore.SKIP_UNIT)
+    rep = stats.run_battery(factory(unit9), budget=10_000_000)
+    assert not rep.errors, rep.errors
+    assert [r.name for r in rep.reports if not r.pass_1e6] == []
+    unit1 = rsacore.make_params(p.p1, p.p2, 1, p.skip, skip_mode=rsacore.SKIP_UNIT, test_mode=True)
+    weak = stats.run_battery(factory(unit1), budget=10_000_000, tests=["frequency", "serial_d2", "max_of_t"])
+    assert not weak.all_pass

@@ -430,3 +430,15 @@ def test_vector_snapshot_restore_and_jump(p0):
     for g in range(4):
         st = rsacore.GeneratorState(m1=3 * p0.b % p0.p1, m2=3 * p0.b % p0.p2, s=int(seeds[g]))
         assert got[:, g].tolist() == rsacore.take_raws(st, p0, 8)
+
+
+@pytest.mark.parametrize("mv", [1, 2, 8, 64])
+def test_vector_equals_interleaved_scalar_streams(p0, mv):
+    """Reference acceptance c09 (test_acceptance.py:192-206): take_floats at Mv
+    equals the block-major interleave of Mv scalar streams seeded with the lane
+    offsets, 10^5 blocks, bit-exact."""
+    blocks = 100_000
+    got = u64np(R.take_floats(R.init_vector(p0, mv=mv), blocks * mv))
+    seeds = [int(x) for x in u64np(skipgen.lane_offset_seeds(p0.skip, 1, mv))]
+    lanes = [np.asarray(rsacore.take_floats(rsacore.init(p0, 0, s0), p0, blocks)) for s0 in seeds]
+    assert np.array_equal(got, np.array(lanes).T.reshape(-1))
