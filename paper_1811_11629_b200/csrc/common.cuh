@@ -25,4 +25,9 @@ inline unsigned grid_for(uint64_t threads, unsigned block) {
     return (unsigned)((threads + block - 1) / block);
 }
 
+// One-thread-per-item launches must fit the 2^31 - 1 grid.x limit.
+inline bool grid_fits(uint64_t threads, unsigned block) {
+    return (threads + block - 1) / block <= 0x7FFFFFFFull;
+}
+
 }  // namespace rsa

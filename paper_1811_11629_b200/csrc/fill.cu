@@ -192,6 +192,7 @@ extern "C" int rsa_fill(const rsa_instance* inst, uint32_t n_inst, uint32_t mv, 
     uint64_t lanes = (uint64_t)n_inst * mv;
     if (n_inst > 1 && (raw_out || f64_out) && inst_stride < blocks * (uint64_t)mv) return RSA_EINVAL;
     if (blocks == 0) return RSA_OK;
+    if (!grid_fits(lanes, 256)) return RSA_EINVAL;
     cudaStream_t st = as_stream(stream);
     if ((flags & RSA_FLAG_FAST) && !(flags & RSA_FLAG_GENERAL_PATH)) {
         // two lanes per thread needs even mv and 16-byte aligned output rows
@@ -225,6 +226,7 @@ extern "C" int rsa_init_lanes(const rsa_instance* inst, uint32_t n_inst, uint32_
                               uint64_t* m1, uint64_t* m2, uint64_t* s, void* stream) {
     if (!inst || !m1 || !m2 || !s || n_inst == 0 || mv == 0) return RSA_EINVAL;
     uint64_t lanes = (uint64_t)n_inst * mv;
+    if (!grid_fits(lanes, 128)) return RSA_EINVAL;
     k_init_lanes<<<grid_for(lanes, 128), 128, 0, as_stream(stream)>>>(inst, mv, lanes, m0_lo, m0_hi,
                                                                        s0, m1, m2, s);
     return launch_status("rsa_init_lanes");

@@ -222,6 +222,7 @@ extern "C" int rsa_fill_segmented(const rsa_instance* inst, uint32_t n_inst, uin
     uint32_t* sums = reinterpret_cast<uint32_t*>(st0 + lanes);
     cudaStream_t st = as_stream(stream);
     const uint64_t threads = lanes * nseg_eff;
+    if (!grid_fits(threads, 256)) return RSA_EINVAL;
     k_seg_sums<<<grid_for(threads, 256), 256, 0, st>>>(inst, mv, lanes, blocks, L, nseg_eff, m1, m2, s, st0, sums);
     int rc = launch_status("rsa_fill_segmented(sums)");
     if (rc) return rc;

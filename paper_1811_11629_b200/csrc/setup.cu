@@ -190,6 +190,7 @@ extern "C" int rsa_setup_instances(const rsa_setup_config* cfg, uint64_t count,
     if (!cfg || !sp || !p1tab || !out || !status || count == 0) return RSA_EINVAL;
     if (cfg->k_p1 == 0 || cfg->k_p2 == 0 || cfg->n_mult == 0 || cfg->e == 0 || cfg->q < 3) return RSA_EINVAL;
     if (!cfg->multiplier && !mult_table) return RSA_EINVAL;
+    if (!grid_fits(count, 128)) return RSA_EINVAL;
     k_setup<<<grid_for(count, 128), 128, 0, as_stream(stream)>>>(*cfg, count, mult_table, sp, n_sp, sp_index,
                                                                 p1tab, n_p1tab, out, status, step_out);
     return launch_status("rsa_setup_instances");
@@ -200,6 +201,7 @@ extern "C" int rsa_find_pair(const uint32_t* p1, uint64_t count, uint64_t q, uin
                              int32_t* status, void* stream) {
     if (!p1 || !sp || !p2 || !status) return RSA_EINVAL;
     if (count == 0) return RSA_OK;
+    if (!grid_fits(count, 128)) return RSA_EINVAL;
     k_find_pair<<<grid_for(count, 128), 128, 0, as_stream(stream)>>>(p1, count, q, tol, sp, n_sp, sp_index,
                                                                      p2, status);
     return launch_status("rsa_find_pair");
