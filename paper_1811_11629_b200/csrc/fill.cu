@@ -31,8 +31,11 @@ RSA_DEV void store_f64(double* p, const double (&v)[LPT]) {
 // On B200 IMAD.WIDE / IMAD.HI (2 slots) and FP64 ops (1 slot) share one
 // 64-slot/clk/SM datapath (profiles/r01_probe_hybrid.txt): a Montgomery
 // product costs 5 slots, a REDC 3, the skip 6, the float map 5.
+#ifndef RSA_FILL_BLOCK
+#define RSA_FILL_BLOCK 128
+#endif
 template <uint32_t E, int LPT, bool RAW, bool F64>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(RSA_FILL_BLOCK)
 k_fill_fast(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t total_lanes,
             uint64_t blocks, uint64_t* __restrict__ m1, uint64_t* __restrict__ m2,
             uint64_t* __restrict__ s, uint64_t* __restrict__ raw, double* __restrict__ f64,
@@ -162,13 +165,13 @@ static void launch_fast(unsigned grid, cudaStream_t st, const rsa_instance* inst
                         uint64_t lanes, uint64_t blocks, uint64_t* m1, uint64_t* m2, uint64_t* s,
                         uint64_t* raw, double* f64, uint64_t stride) {
     if (raw && f64)
-        k_fill_fast<E, LPT, true, true><<<grid, 256, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride);
+        k_fill_fast<E, LPT, true, true><<<grid, RSA_FILL_BLOCK, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride);
     else if (raw)
-        k_fill_fast<E, LPT, true, false><<<grid, 256, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride);
+        k_fill_fast<E, LPT, true, false><<<grid, RSA_FILL_BLOCK, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride);
     else if (f64)
-        k_fill_fast<E, LPT, false, true><<<grid, 256, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride);
+        k_fill_fast<E, LPT, false, true><<<grid, RSA_FILL_BLOCK, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride);
     else
-        k_fill_fast<E, LPT, false, false><<<grid, 256, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride);
+        k_fill_fast<E, LPT, false, false><<<grid, RSA_FILL_BLOCK, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride);
 }
 
 template <int LPT>
@@ -192,7 +195,7 @@ extern "C" int rsa_fill(const rsa_instance* inst, uint32_t n_inst, uint32_t mv, 
     uint64_t lanes = (uint64_t)n_inst * mv;
     if (n_inst > 1 && (raw_out || f64_out) && inst_stride < blocks * (uint64_t)mv) return RSA_EINVAL;
     if (blocks == 0) return RSA_OK;
-    if (!grid_fits(lanes, 256)) return RSA_EINVAL;
+    if (!grid_fits(lanes, RSA_FILL_BLOCK)) return RSA_EINVAL;
     cudaStream_t st = as_stream(stream);
     if ((flags & RSA_FLAG_FAST) && !(flags & RSA_FLAG_GENERAL_PATH)) {
         // two lanes per thread needs even mv and 16-byte aligned output rows
@@ -200,9 +203,9 @@ extern "C" int rsa_fill(const rsa_instance* inst, uint32_t n_inst, uint32_t mv, 
                     ((uintptr_t)raw_out % 16 == 0) && ((uintptr_t)f64_out % 16 == 0) &&
                     !(flags & RSA_FLAG_ONE_LANE);
         if (pair)
-            dispatch_e<2>(e, grid_for(lanes / 2, 256), st, inst, mv, lanes, blocks, m1, m2, s, raw_out, f64_out, inst_stride);
+            dispatch_e<2>(e, grid_for(lanes / 2, RSA_FILL_BLOCK), st, inst, mv, lanes, blocks, m1, m2, s, raw_out, f64_out, inst_stride);
         else
-            dispatch_e<1>(e, grid_for(lanes, 256), st, inst, mv, lanes, blocks, m1, m2, s, raw_out, f64_out, inst_stride);
+            dispatch_e<1>(e, grid_for(lanes, RSA_FILL_BLOCK), st, inst, mv, lanes, blocks, m1, m2, s, raw_out, f64_out, inst_stride);
         return launch_status("rsa_fill(fast)");
     }
     k_fill_general<<<grid_for(lanes, 256), 256, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw_out,
