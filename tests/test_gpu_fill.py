@@ -442,3 +442,34 @@ def test_vector_equals_interleaved_scalar_streams(p0, mv):
     seeds = [int(x) for x in u64np(skipgen.lane_offset_seeds(p0.skip, 1, mv))]
     lanes = [np.asarray(rsacore.take_floats(rsacore.init(p0, 0, s0), p0, blocks)) for s0 in seeds]
     assert np.array_equal(got, np.array(lanes).T.reshape(-1))
+
+
+@pytest.mark.parametrize("mv,blocks,stride_pad", [(1, 20000, 0), (5, 4000, 3), (64, 9000, 16)])
+def test_segmented_multi_instance(golden_streams, mv, blocks, stride_pad):
+    """rsa_fill_segmented with n_inst > 1 (instance-major rows, padded
+    strides) equals rsa_fill on the same lanes, outputs and final state."""
+    from paper_1811_11629_b200 import _device
+    t = R.derive_params_table(golden_streams["master_seed"], 3, 4)
+    d = t.device
+    lib = _lib.load()
+    lanes = 4 * mv
+    assert lib.rsa_fill_segments(lanes, blocks) > 1
+    stride = blocks * mv + stride_pad
+    res = []
+    for seg in (False, True):
+        m1, m2, s = vecgen._init_lanes(t.inst, 4, mv, 424242, 7, d)
+        raw = torch.zeros(4 * stride, dtype=torch.uint64, device=d)
+        f = torch.full((4 * stride,), -1.0, dtype=torch.float64, device=d)
+        args = (t.inst.data_ptr(), 4, mv, blocks, 9, _lib.RSA_FLAG_FAST, m1.data_ptr(), m2.data_ptr(),
+                s.data_ptr(), raw.data_ptr(), f.data_ptr(), stride)
+        if seg:
+            nb = int(lib.rsa_fill_segmented_scratch_bytes(lanes, blocks))
+            sc = torch.empty(nb, dtype=torch.uint8, device=d)
+            _lib.call("rsa_fill_segmented", *args, sc.data_ptr(), nb, _device.stream(d))
+        else:
+            _lib.call("rsa_fill", *args, _device.stream(d))
+        res.append([u64np(x) for x in (raw, f, m1, m2, s)])
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)
+    f = res[1][1].reshape(4, stride)
+    assert (f[:, blocks * mv:] == -1.0).all()
