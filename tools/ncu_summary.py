@@ -65,8 +65,10 @@ def main():
             traffic[f"fill_e{mt.group(1)}"] = rd + wr
         elif "k_fused" in name:
             traffic["fused"] = rd + wr
-        elif "k_scan_flags" in name:
-            traffic["scan"] = rd + wr
+        elif "k_scan_sieve" in name:
+            traffic["scan_sieve"] = rd + wr
+        elif "k_setup" in name:
+            traffic["setup"] = rd + wr
     with open(out_md, "w") as fh:
         fh.write("\n".join(lines) + "\n")
     with open(tpath, "w") as fh:
