@@ -49,6 +49,8 @@ extern "C" {
 #define RSA_FLAG_FIXED 2u  /* unit / const skip: per-lane skip register is constant     */
 #define RSA_FLAG_GENERAL_PATH 4u /* rsa_fill hint: force the general kernel (cross-checks) */
 #define RSA_FLAG_ONE_LANE 8u     /* rsa_fill hint: one lane per thread (tuning / A-B)       */
+#define RSA_FLAG_INTERLEAVE 16u  /* rsa_fill: instances round-robin, draw t of i at out[t*n_inst+i] */
+#define RSA_FLAG_LOW32 32u       /* rsa_fill: f64_out = (c mod 2^32) / 2^32 instead of the float map */
 
 /*
  * Per-instance constants, 128 bytes, one per generator instance.  The first
@@ -95,6 +97,12 @@ typedef struct rsa_instance {
  * general kernel (test-mode sizes, any prime q, unit/const skips) runs.
  * RSA_FLAG_GENERAL_PATH forces the general kernel (independent cross-check);
  * RSA_FLAG_ONE_LANE forces one lane per thread.
+ * RSA_FLAG_INTERLEAVE (fast path): the n_inst streams are written round-robin,
+ * draw t = k*mv + g of instance i at out[t*n_inst + i] (inst_stride unused) —
+ * the interleaved multi-stream source of stats.BitSource (stats.py:118-136).
+ * RSA_FLAG_LOW32 (fast path): f64_out holds (c mod 2^32) * 2^-32, the
+ * BitSource "raw_low_bits" view, instead of the float map.
+ * The general path returns RSA_EPARAMS for either layout flag.
  * --------------------------------------------------------------------------- */
 int rsa_fill(const rsa_instance* inst, uint32_t n_inst, uint32_t mv, uint64_t blocks,
              uint32_t e, uint32_t flags, uint64_t* m1, uint64_t* m2, uint64_t* s,

@@ -30,6 +30,7 @@ RSA_EALIGN = -5
 RSA_SKIP_LCG, RSA_SKIP_UNIT, RSA_SKIP_CONST = 0, 1, 2
 RSA_BT_HIST, RSA_BT_SERIAL, RSA_BT_POKER, RSA_BT_MAX_OF_T, RSA_BT_PERMUTATION, RSA_BT_COLLISION = 1, 2, 3, 4, 5, 6
 RSA_FLAG_FAST, RSA_FLAG_FIXED, RSA_FLAG_GENERAL_PATH, RSA_FLAG_ONE_LANE = 1, 2, 4, 8
+RSA_FLAG_INTERLEAVE, RSA_FLAG_LOW32 = 16, 32
 
 # rsa_instance (128 bytes) — field order and offsets mirror the C struct.
 INSTANCE_DTYPE = np.dtype({

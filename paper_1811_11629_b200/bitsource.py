@@ -6,8 +6,11 @@ Selectors: 'float_leading' (the stream doubles), 'raw_low_bits' (low 32 bits
 of the raw ciphertexts scaled to [0, 1)), 'raw_word' (the raw uint64 words).
 Several streams are interleaved round-robin by draw index, stream 0 first,
 with the same surplus buffering as the reference.  Everything stays on the
-device: each stream's block fill runs in K1, the views and the round-robin
-transpose are device tensor ops.
+device.  When the streams share Mv, exponent and the fast kernel, whole
+blocks come from ONE K1 launch that writes the round-robin order and the
+selector's view directly (RSA_FLAG_INTERLEAVE / RSA_FLAG_LOW32; the streams'
+lane arrays become views of one combined array); partial blocks and pending
+draws take the per-stream path (take_raw, view, device transpose).
 """
 
 from __future__ import annotations
@@ -16,7 +19,8 @@ from typing import Sequence
 
 import torch
 
-from . import paramfactory, vecgen
+from . import _device, _lib, paramfactory, vecgen
+from .rsacore import device_instance, instance_flags
 from .vecgen import VectorState
 
 SELECTORS = ("float_leading", "raw_low_bits", "raw_word")
@@ -35,6 +39,28 @@ class BitSource:
         self.streams = list(streams)
         self.selector = selector
         self._buffer: torch.Tensor | None = None
+        self._fused = self._setup_fused()
+
+    def _setup_fused(self) -> tuple | None:
+        """(instance table, m1, m2, s) for the one-launch interleaved fill, or
+        None when the streams do not share one fast kernel configuration."""
+        st = self.streams
+        if len(st) < 2 or len({id(x) for x in st}) != len(st):
+            return None
+        p0 = st[0].params
+        if any(x.mv != st[0].mv or x.params.e != p0.e or x.device != st[0].device for x in st):
+            return None
+        if not all(instance_flags(x.params) & _lib.RSA_FLAG_FAST for x in st):
+            return None
+        d = st[0].device
+        inst = torch.cat([device_instance(x.params, d) for x in st]).contiguous()
+        comb = []
+        for name in ("m1", "m2", "s"):
+            t = torch.cat([getattr(x, name) for x in st]).contiguous()
+            for i, x in enumerate(st):  # the streams keep working on views of the combined lanes
+                setattr(x, name, t[i * x.mv:(i + 1) * x.mv])
+            comb.append(t)
+        return (inst, *comb)
 
     def _view(self, raw: torch.Tensor, state: VectorState) -> torch.Tensor:
         if self.selector == "float_leading":
@@ -59,12 +85,54 @@ class BitSource:
             have = head.numel()
         if have < count:
             rounds = -(-(count - have) // k)
-            views = [self._view(vecgen.take_raw(st, rounds), st) for st in self.streams]
-            flat = torch.stack(views).T.reshape(-1)
+            flat = self._rounds(rounds)
             need = count - have
             parts.append(flat[:need])
             self._buffer = flat[need:]
         return parts[0] if len(parts) == 1 else torch.cat(parts)
+
+
+    def _per_stream(self, rounds: int) -> torch.Tensor:
+        views = [self._view(vecgen.take_raw(st, rounds), st) for st in self.streams]
+        return torch.stack(views).T.reshape(-1)
+
+    def _rounds(self, rounds: int) -> torch.Tensor:
+        """`rounds` draws of every stream, interleaved (rounds * k values)."""
+        st = self.streams
+        k = len(st)
+        pend = [x._pending.numel() for x in st]
+        mv = st[0].mv
+        if self._fused is None or len(set(pend)) != 1 or (rounds - min(pend[0], rounds)) < mv:
+            return self._per_stream(rounds)
+        dev = st[0].device
+        dtype = torch.uint64 if self.selector == "raw_word" else torch.float64
+        res = torch.empty(rounds * k, dtype=dtype, device=dev)
+        pos = min(pend[0], rounds)  # pending draws first (equal across the streams)
+        if pos:
+            res[:pos * k] = self._per_stream(pos)
+        nb = (rounds - pos) // mv
+        L = _lib.load()
+        if int(L.rsa_fill_segments(k * mv, nb)) > 1:  # too few lanes: per-stream segmented fills
+            res[pos * k:(pos + nb * mv) * k] = self._per_stream(nb * mv)
+        else:
+            inst, m1, m2, s = self._fused
+            seg = res[pos * k:(pos + nb * mv) * k]
+            flags = _lib.RSA_FLAG_FAST | _lib.RSA_FLAG_INTERLEAVE
+            raw = f64 = None
+            if self.selector == "raw_word":
+                raw = seg.data_ptr()
+            else:
+                f64 = seg.data_ptr()
+                if self.selector == "raw_low_bits":
+                    flags |= _lib.RSA_FLAG_LOW32
+            _lib.call("rsa_fill", inst.data_ptr(), k, mv, nb, st[0].params.e, flags, m1.data_ptr(),
+                      m2.data_ptr(), s.data_ptr(), raw, f64, 0, _device.stream(dev))
+            for x in st:
+                x.draws += nb * mv
+        pos += nb * mv
+        if rounds > pos:
+            res[pos * k:] = self._per_stream(rounds - pos)
+        return res
 
 
 def interstream_params(master_seed: int, first_stream: int, m_p: int, e: int = 9, dev=None):

@@ -34,30 +34,48 @@ RSA_DEV void store_f64(double* p, const double (&v)[LPT]) {
 #ifndef RSA_FILL_BLOCK
 #define RSA_FILL_BLOCK 128
 #endif
-template <uint32_t E, int LPT, bool RAW, bool F64>
+// F64: 0 = no float output, 1 = the float map, 2 = low 32 bits / 2^32
+// (stats.BitSource's raw_low_bits selector, stats.py:118-136).  ilv != 0: the
+// n_inst = ilv instances are interleaved round-robin, draw t of instance i at
+// out[t*ilv + i] (LPT = 1 only).
+template <uint32_t E, int LPT, bool RAW, int F64>
 __global__ void __launch_bounds__(RSA_FILL_BLOCK)
 k_fill_fast(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t total_lanes,
             uint64_t blocks, uint64_t* __restrict__ m1, uint64_t* __restrict__ m2,
             uint64_t* __restrict__ s, uint64_t* __restrict__ raw, double* __restrict__ f64,
-            uint64_t inst_stride) {
+            uint64_t inst_stride, uint32_t ilv) {
     uint64_t lane = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * LPT;
     if (lane >= total_lanes) return;
-    uint64_t i = lane / mv;
-    uint32_t g = (uint32_t)(lane - i * mv);
+    uint64_t i;
+    uint32_t g;
+    if (LPT == 1 && ilv) {  // instance fastest across threads: a warp's stores are contiguous
+        g = (uint32_t)(lane / ilv);
+        i = lane - (uint64_t)g * ilv;
+        lane = i * mv + g;
+    } else {
+        i = lane / mv;
+        g = (uint32_t)(lane - i * mv);
+    }
     const FastInst P = load_fast(inst + i);
     Lane L[LPT];
 #pragma unroll
     for (int j = 0; j < LPT; ++j) L[j] = lane_in(P, m1[lane + j], m2[lane + j], s[lane + j]);
-    uint64_t off = i * inst_stride + g;
-    for (uint64_t k = 0; k < blocks; ++k, off += mv) {
+    uint64_t off = i * inst_stride + g, step = mv;
+    if (LPT == 1 && ilv) {
+        off = (uint64_t)g * ilv + i;
+        step = (uint64_t)mv * ilv;
+    }
+    for (uint64_t k = 0; k < blocks; ++k, off += step) {
         uint64_t c[LPT];
 #pragma unroll
         for (int j = 0; j < LPT; ++j) c[j] = draw_fast<E>(P, L[j]);
         if constexpr (RAW) store_u64<LPT>(raw + off, c);
-        if constexpr (F64) {
+        if constexpr (F64 != 0) {
             double r[LPT];
 #pragma unroll
-            for (int j = 0; j < LPT; ++j) r[j] = to_unit(c[j], P.n_float, P.n_recip, P.n_recip_lo);
+            for (int j = 0; j < LPT; ++j)
+                r[j] = F64 == 1 ? to_unit(c[j], P.n_float, P.n_recip, P.n_recip_lo)
+                                : __uint2double_rn((uint32_t)c[j]) * 0x1p-32;
             store_f64<LPT>(f64 + off, r);
         }
     }
@@ -163,28 +181,32 @@ using namespace rsa;
 template <uint32_t E, int LPT>
 static void launch_fast(unsigned grid, cudaStream_t st, const rsa_instance* inst, uint32_t mv,
                         uint64_t lanes, uint64_t blocks, uint64_t* m1, uint64_t* m2, uint64_t* s,
-                        uint64_t* raw, double* f64, uint64_t stride) {
-    if (raw && f64)
-        k_fill_fast<E, LPT, true, true><<<grid, RSA_FILL_BLOCK, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride);
-    else if (raw)
-        k_fill_fast<E, LPT, true, false><<<grid, RSA_FILL_BLOCK, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride);
-    else if (f64)
-        k_fill_fast<E, LPT, false, true><<<grid, RSA_FILL_BLOCK, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride);
-    else
-        k_fill_fast<E, LPT, false, false><<<grid, RSA_FILL_BLOCK, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride);
+                        uint64_t* raw, double* f64, uint64_t stride, uint32_t ilv, bool low32) {
+#define RSA_LAUNCH(R, F) k_fill_fast<E, LPT, R, F><<<grid, RSA_FILL_BLOCK, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride, ilv)
+    if constexpr (LPT == 1) {
+        if (f64 && low32) {
+            if (raw) RSA_LAUNCH(true, 2); else RSA_LAUNCH(false, 2);
+            return;
+        }
+    }
+    if (raw && f64) RSA_LAUNCH(true, 1);
+    else if (raw) RSA_LAUNCH(true, 0);
+    else if (f64) RSA_LAUNCH(false, 1);
+    else RSA_LAUNCH(false, 0);
+#undef RSA_LAUNCH
 }
 
 template <int LPT>
 static void dispatch_e(uint32_t e, unsigned grid, cudaStream_t st, const rsa_instance* inst,
                        uint32_t mv, uint64_t lanes, uint64_t blocks, uint64_t* m1, uint64_t* m2,
-                       uint64_t* s, uint64_t* raw, double* f64, uint64_t stride) {
+                       uint64_t* s, uint64_t* raw, double* f64, uint64_t stride, uint32_t ilv, bool low32) {
     switch (e) {
-        case 3: launch_fast<3, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride); break;
-        case 5: launch_fast<5, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride); break;
-        case 9: launch_fast<9, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride); break;
-        case 17: launch_fast<17, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride); break;
-        case 65537: launch_fast<65537, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride); break;
-        default: launch_fast<0, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride); break;
+        case 3: launch_fast<3, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride, ilv, low32); break;
+        case 5: launch_fast<5, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride, ilv, low32); break;
+        case 9: launch_fast<9, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride, ilv, low32); break;
+        case 17: launch_fast<17, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride, ilv, low32); break;
+        case 65537: launch_fast<65537, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride, ilv, low32); break;
+        default: launch_fast<0, LPT>(grid, st, inst, mv, lanes, blocks, m1, m2, s, raw, f64, stride, ilv, low32); break;
     }
 }
 
@@ -193,7 +215,8 @@ extern "C" int rsa_fill(const rsa_instance* inst, uint32_t n_inst, uint32_t mv, 
                         uint64_t* raw_out, double* f64_out, uint64_t inst_stride, void* stream) {
     if (!inst || !m1 || !m2 || !s || n_inst == 0 || mv == 0 || e == 0) return RSA_EINVAL;
     uint64_t lanes = (uint64_t)n_inst * mv;
-    if (n_inst > 1 && (raw_out || f64_out) && inst_stride < blocks * (uint64_t)mv) return RSA_EINVAL;
+    const bool ilv = flags & RSA_FLAG_INTERLEAVE, low32 = flags & RSA_FLAG_LOW32;
+    if (n_inst > 1 && !ilv && (raw_out || f64_out) && inst_stride < blocks * (uint64_t)mv) return RSA_EINVAL;
     if (blocks == 0) return RSA_OK;
     if (!grid_fits(lanes, RSA_FILL_BLOCK)) return RSA_EINVAL;
     cudaStream_t st = as_stream(stream);
@@ -201,13 +224,16 @@ extern "C" int rsa_fill(const rsa_instance* inst, uint32_t n_inst, uint32_t mv, 
         // two lanes per thread needs even mv and 16-byte aligned output rows
         bool pair = (mv % 2 == 0) && (n_inst == 1 || inst_stride % 2 == 0) &&
                     ((uintptr_t)raw_out % 16 == 0) && ((uintptr_t)f64_out % 16 == 0) &&
-                    !(flags & RSA_FLAG_ONE_LANE);
+                    !(flags & RSA_FLAG_ONE_LANE) && !ilv && !low32;
         if (pair)
-            dispatch_e<2>(e, grid_for(lanes / 2, RSA_FILL_BLOCK), st, inst, mv, lanes, blocks, m1, m2, s, raw_out, f64_out, inst_stride);
+            dispatch_e<2>(e, grid_for(lanes / 2, RSA_FILL_BLOCK), st, inst, mv, lanes, blocks, m1, m2, s, raw_out,
+                          f64_out, inst_stride, 0, false);
         else
-            dispatch_e<1>(e, grid_for(lanes, RSA_FILL_BLOCK), st, inst, mv, lanes, blocks, m1, m2, s, raw_out, f64_out, inst_stride);
+            dispatch_e<1>(e, grid_for(lanes, RSA_FILL_BLOCK), st, inst, mv, lanes, blocks, m1, m2, s, raw_out,
+                          f64_out, inst_stride, ilv ? n_inst : 0, low32);
         return launch_status("rsa_fill(fast)");
     }
+    if (ilv || low32) return RSA_EPARAMS;  // layouts of the fast kernel only
     k_fill_general<<<grid_for(lanes, 256), 256, 0, st>>>(inst, mv, lanes, blocks, m1, m2, s, raw_out,
                                                         f64_out, inst_stride);
     return launch_status("rsa_fill(general)");

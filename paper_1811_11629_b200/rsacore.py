@@ -107,21 +107,37 @@ def _root_factors(q: int):
     return Q_DEFAULT_FACTORS if q == Q_DEFAULT else None
 
 
+# The number-theoretic checks are pure functions of their integers; streams are
+# re-validated on every init / init_vector, so they are memoised.
+@functools.lru_cache(maxsize=1 << 14)
+def _is_safe_prime(p: int) -> bool:
+    return numtheory.is_safe_prime(p)
+
+
+@functools.lru_cache(maxsize=1 << 10)
+def _is_prime64(q: int) -> bool:
+    return numtheory.is_prime64(q)
+
+
+@functools.lru_cache(maxsize=1 << 12)
+def _is_primitive_root(a: int, q: int) -> bool:
+    return numtheory.is_primitive_root(a, q, _root_factors(q))
+
+
 def validate_params(params: GeneratorParams) -> None:
     """Raise InvalidParams naming the first violated invariant (rsacore.py:117-181)."""
     p1, p2, n, e, sk = params.p1, params.p2, params.n, params.e, params.skip
     checks = (
         (p1 == p2, "p1 == p2"),
         (n != p1 * p2, "n != p1*p2"),
-        (lambda: not numtheory.is_safe_prime(p1), f"p1={p1} is not a safe prime"),
-        (lambda: not numtheory.is_safe_prime(p2), f"p2={p2} is not a safe prime"),
+        (lambda: not _is_safe_prime(p1), f"p1={p1} is not a safe prime"),
+        (lambda: not _is_safe_prime(p2), f"p2={p2} is not a safe prime"),
         (e < 1 or e % 2 == 0, f"exponent e={e} must be odd and positive"),
         (e > MAX_EXPONENT, f"exponent e={e} above {MAX_EXPONENT}"),
-        (lambda: not numtheory.is_prime64(sk.q), f"q={sk.q} is not prime"),
+        (lambda: not _is_prime64(sk.q), f"q={sk.q} is not prime"),
         (sk.a * sk.a > sk.q, "multiplier violates a*a <= q"),
         (sk.q1 != sk.q // sk.a or sk.q2 != sk.q % sk.a, "inconsistent Schrage constants q1/q2"),
-        (lambda: not numtheory.is_primitive_root(sk.a, sk.q, _root_factors(sk.q)),
-         f"a={sk.a} is not a primitive root mod q"),
+        (lambda: not _is_primitive_root(sk.a, sk.q), f"a={sk.a} is not a primitive root mod q"),
         (math.gcd(n, sk.q) != 1, "gcd(n, q) != 1"),
         (math.gcd(n, sk.q - 1) != 1, "gcd(n, q-1) != 1"),
         (params.b != sk.q * (sk.q - 1) // 2 % n, "inconsistent period offset b"),
