@@ -29,8 +29,11 @@ RSA_DEV void flush_hist(uint16_t* h, uint32_t* gh, bool active) {
     }
 }
 
+#ifndef RSA_FUSED_MINB
+#define RSA_FUSED_MINB 8
+#endif
 template <uint32_t E>
-__global__ void __launch_bounds__(FUSED_BLOCK, 8)
+__global__ void __launch_bounds__(FUSED_BLOCK, RSA_FUSED_MINB)
 k_fused(const rsa_instance* __restrict__ inst, uint32_t n_inst, uint64_t draws,
         uint64_t* __restrict__ m1, uint64_t* __restrict__ m2, uint64_t* __restrict__ s,
         rsa_fused_stat* __restrict__ stats, uint32_t* __restrict__ hist) {
