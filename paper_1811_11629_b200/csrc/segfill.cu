@@ -71,10 +71,18 @@ k_seg_sums(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t lanes, u
 }
 
 // Exclusive scan over the segments of each lane (in place), mod p1 / p2:
-// one CTA per lane, each thread reduces a run of consecutive segments, a
-// block scan (warp shuffles + one smem pass) combines the runs, and each
-// thread rewrites its run with the running prefix.  Modular addition is
-// associative, so the result equals the sequential scan.
+// one CTA per lane, warp w owns a contiguous run of segments and walks it 32
+// at a time (coalesced loads, a shuffle scan per step, a running carry); the
+// warp totals are scanned once more and added on the way out.  Modular
+// addition is associative, so the result equals the sequential scan.
+RSA_DEV void warp_scan2(uint32_t& v1, uint32_t& v2, uint32_t p1, uint32_t p2, int wl) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o1 = __shfl_up_sync(0xffffffffu, v1, d), o2 = __shfl_up_sync(0xffffffffu, v2, d);
+        if (wl >= d) { v1 = add_mod(v1, o1, p1); v2 = add_mod(v2, o2, p2); }
+    }
+}
+
 __global__ void __launch_bounds__(1024)
 k_seg_scan_block(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t lanes, uint64_t nseg,
                  uint32_t* __restrict__ sums) {
@@ -82,45 +90,45 @@ k_seg_scan_block(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t la
     const uint64_t lane = blockIdx.x;
     const rsa_instance* ip = inst + lane / mv;
     const uint32_t p1 = ip->p1, p2 = ip->p2;
-    const uint64_t per = (nseg + blockDim.x - 1) / blockDim.x;
-    const uint64_t j0 = threadIdx.x * per, j1 = min(nseg, j0 + per);
-    uint32_t a1 = 0, a2 = 0;
-    for (uint64_t j = j0; j < j1; ++j) {
+    const int wl = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint64_t per = (nseg + nw - 1) / nw;  // segments per warp
+    const uint64_t j0 = (uint64_t)wid * per, j1 = min(nseg, j0 + per);
+    // pass 1: warp totals
+    uint32_t t1 = 0, t2 = 0;
+    for (uint64_t j = j0 + wl; j < j1; j += 32) {
         const uint64_t t = j * lanes + lane;
-        a1 = add_mod(a1, sums[2 * t], p1);
-        a2 = add_mod(a2, sums[2 * t + 1], p2);
+        t1 = add_mod(t1, sums[2 * t], p1);
+        t2 = add_mod(t2, sums[2 * t + 1], p2);
     }
-    // inclusive scan of (a1, a2) over the threads
-    const int wl = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-    uint32_t i1 = a1, i2 = a2;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t o1 = __shfl_up_sync(0xffffffffu, i1, d), o2 = __shfl_up_sync(0xffffffffu, i2, d);
-        if (wl >= d) { i1 = add_mod(i1, o1, p1); i2 = add_mod(i2, o2, p2); }
+    for (int d = 16; d > 0; d >>= 1) {
+        t1 = add_mod(t1, __shfl_xor_sync(0xffffffffu, t1, d), p1);
+        t2 = add_mod(t2, __shfl_xor_sync(0xffffffffu, t2, d), p2);
     }
-    if (wl == 31) { w1[wid] = i1; w2[wid] = i2; }
+    if (wl == 0) { w1[wid] = t1; w2[wid] = t2; }
     __syncthreads();
-    if (wid == 0) {
+    if (wid == 0) {  // exclusive scan of the warp totals
         uint32_t x1 = wl < nw ? w1[wl] : 0, x2 = wl < nw ? w2[wl] : 0;
         uint32_t y1 = x1, y2 = x2;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t o1 = __shfl_up_sync(0xffffffffu, y1, d), o2 = __shfl_up_sync(0xffffffffu, y2, d);
-            if (wl >= d) { y1 = add_mod(y1, o1, p1); y2 = add_mod(y2, o2, p2); }
-        }
-        if (wl < nw) { w1[wl] = sub_mod(y1, x1, p1); w2[wl] = sub_mod(y2, x2, p2); }  // exclusive
+        warp_scan2(y1, y2, p1, p2, wl);
+        if (wl < nw) { w1[wl] = sub_mod(y1, x1, p1); w2[wl] = sub_mod(y2, x2, p2); }
     }
     __syncthreads();
-    // exclusive prefix of this thread's run
-    uint32_t r1 = add_mod(w1[wid], sub_mod(i1, a1, p1), p1);
-    uint32_t r2 = add_mod(w2[wid], sub_mod(i2, a2, p2), p2);
-    for (uint64_t j = j0; j < j1; ++j) {
+    // pass 2: rewrite each run with its exclusive prefix, 32 segments per step
+    uint32_t c1 = w1[wid], c2 = w2[wid];
+    for (uint64_t base = j0; base < j1; base += 32) {
+        const uint64_t j = base + wl;
+        const bool in = j < j1;
         const uint64_t t = j * lanes + lane;
-        const uint32_t v1 = sums[2 * t], v2 = sums[2 * t + 1];
-        sums[2 * t] = r1;
-        sums[2 * t + 1] = r2;
-        r1 = add_mod(r1, v1, p1);
-        r2 = add_mod(r2, v2, p2);
+        const uint32_t v1 = in ? sums[2 * t] : 0, v2 = in ? sums[2 * t + 1] : 0;
+        uint32_t i1 = v1, i2 = v2;
+        warp_scan2(i1, i2, p1, p2, wl);
+        if (in) {
+            sums[2 * t] = add_mod(c1, sub_mod(i1, v1, p1), p1);
+            sums[2 * t + 1] = add_mod(c2, sub_mod(i2, v2, p2), p2);
+        }
+        c1 = add_mod(c1, __shfl_sync(0xffffffffu, i1, 31), p1);
+        c2 = add_mod(c2, __shfl_sync(0xffffffffu, i2, 31), p2);
     }
 }
 
