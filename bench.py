@@ -411,7 +411,7 @@ def run_gpu(args):
         from bench_configs import run_other
         line = run_other(args, world, rank, local)
     if rank == 0:
-        if not args.no_cpu:
+        if not args.no_cpu and world == 1:  # the CPU baseline is an N=1, rank-0 measurement
             line["cpu_baseline"] = cpu_port_rate()
         print(json.dumps(line), flush=True)
     if world > 1:
