@@ -74,6 +74,8 @@ class FusedConsumer:
         self.draws = 0
 
     def run(self, draws: int) -> FusedStats:
+        if draws < 2:
+            raise ValueError("the fused statistics need at least 2 draws per instance (var uses N-1)")
         d = self.table.device
         n = self.table.count
         stats = torch.empty((n, 6), dtype=torch.float64, device=d)

@@ -65,6 +65,8 @@ def test_fused_rejects_odd_count():
     t = R.derive_params_table(SEED, 0, 3)
     with pytest.raises(ValueError):
         R.FusedConsumer(t)
+    with pytest.raises(ValueError):
+        R.FusedConsumer(R.derive_params_table(SEED, 0, 2)).run(1)
 
 
 def test_many_instance_fill_config3(golden_meta):
