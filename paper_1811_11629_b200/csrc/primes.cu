@@ -120,57 +120,6 @@ RSA_DEV uint32_t r_mod(uint32_t n) {
     return r;
 }
 
-// g R mod n for a small base g by a doubling chain on R mod n (ALU only)
-RSA_DEV uint32_t small_base_m(uint32_t g, uint32_t onem, uint32_t n) {
-    uint32_t x = onem;
-    for (int b = 30 - __clz(g); b >= 0; --b) {
-        x = add_mod(x, x, n);
-        if ((g >> b) & 1u) x = add_mod(x, onem, n);
-    }
-    return x;
-}
-
-// strong probable prime to a small base g (numtheory.py:60-78), Montgomery domain
-RSA_DEV bool sprp_small(uint32_t n, uint32_t g) {
-    const uint32_t ninv = inv32(n), onem = r_mod(n);
-    uint32_t d = n - 1;
-    const int u = __ffs(d) - 1;
-    d >>= u;
-    const uint32_t x = mont_pow_m(small_base_m(g, onem, n), d, onem, n, ninv);
-    const uint32_t minus1 = n - onem;
-    if (x == onem || x == minus1) return true;
-    uint32_t y = x;
-    for (int j = 1; j < u; ++j) {
-        y = mont_mul(y, y, n, ninv);
-        if (y == minus1) return true;
-    }
-    return false;
-}
-
-// Strong probable prime to base 2 (numtheory.py:60-78): left-to-right powering
-// in the Montgomery domain where "multiply by 2" is a modular doubling, so the
-// 31-bit exponent costs only squarings.
-RSA_DEV bool sprp2(uint32_t n) {
-    const uint32_t ninv = inv32(n), onem = r_mod(n);
-    uint32_t d = n - 1;
-    const int u = __ffs(d) - 1;
-    d >>= u;
-    uint32_t x = onem;  // 1 in Montgomery form
-    for (int b = 31 - __clz(d); b >= 0; --b) {
-        x = mont_mul(x, x, n, ninv);
-        if ((d >> b) & 1u) x = add_mod(x, x, n);
-    }
-    const uint32_t minus1 = n - onem;
-    if (x == onem || x == minus1) return true;
-    for (int j = 1; j < u; ++j) {
-        x = mont_mul(x, x, n, ninv);
-        if (x == minus1) return true;
-    }
-    return false;
-}
-
-RSA_DEV bool mr_7_61(uint32_t n) { return sprp_small(n, 7) && sprp_small(n, 61); }
-
 // The 2314 base-2 strong pseudoprimes below 2^32 (tools/gen_spsp2.c, which
 // decides compositeness with the deterministic bases 2, 7, 61).  An n < 2^32
 // that is a base-2 SPRP is prime iff it is not in this table, so the scan's
@@ -213,14 +162,6 @@ RSA_DEV bool is_spsp2(uint32_t n) {
     for (uint32_t k = 0; k < SPSP_MAXB; ++k)
         if (lo + k < hi) hit |= __ldg(&g_spsp.v[lo + k]) == n;
     return hit;
-}
-
-// Safe-prime predicate for one scan candidate (5, 7, or p = 11 mod 12).
-RSA_DEV bool candidate_is_safe(uint32_t p) {
-    if (p < 10201u) return is_safe_prime32(p);  // small: exact generic path
-    uint32_t q = (p - 1) >> 1;                   // odd, not divisible by 3
-    if (has_small_factor(p) || has_small_factor(q)) return false;
-    return sprp2(p) && sprp2(q) && mr_7_61(p) && mr_7_61(q);
 }
 
 struct ScanRange {
@@ -458,7 +399,8 @@ k_scan_sieve(ScanRange R, uint64_t cta0, uint32_t* __restrict__ words, uint32_t*
 // IMAD pipe mostly idle (64 warps x 1 chain cannot cover its latency), K
 // chains per thread give the scheduler K-fold ILP.  Leading zero bits of a
 // shorter exponent square the Montgomery one, which stays one, so all K run
-// the same 32-bit-position loop.  Same verdicts as sprp2().
+// the same 32-bit-position loop.  Verdicts of the strong probable-prime test
+// to base 2 (numtheory.py:60-78), with "multiply by 2" a modular doubling.
 template <int K>
 RSA_DEV void sprp2_multi(const uint32_t (&n)[K], bool (&ok)[K]) {
     uint32_t ninv[K], onem[K], d[K], x[K];
