@@ -413,6 +413,8 @@ def run_gpu(args):
     if rank == 0:
         if not args.no_cpu and world == 1:  # the CPU baseline is an N=1, rank-0 measurement
             line["cpu_baseline"] = cpu_port_rate()
+            one = cpu_port_rate(procs=1)  # also the single-process figure
+            line["cpu_baseline"]["one_process"] = {"value": one["value"], "unit": one["unit"], "cores": 1}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
