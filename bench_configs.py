@@ -172,6 +172,9 @@ def run_other(args, world, rank, local):
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(st)
         sp = paramfactory.safe_primes_u32(lo, hi, dev)
+        if world > 1:  # all-gather the per-rank counts and lists -> the global table
+            from paper_1811_11629_b200.shard import gather_sorted
+            sp = gather_sorted(sp.view(torch.int32))
         e1.record(st)
         R.derive_params_table(R.DEFAULT_MASTER_SEED, first, n, dev=dev)
         e2.record(st)
@@ -185,7 +188,7 @@ def run_other(args, world, rank, local):
     line = _base_line(args, world, cands * args.steps / el / 1e9, el, clk,
                       {"workload": "config5 setup: safe-prime scan (sieve to 8191, base-2 SPRP, spsp(2) table) of all 2^30 odd candidates in "
                                    "[2^31,2^32) + 2^20 instance tuples (ids 0..2^20-1)",
-                       "unit_note": "value = odd candidates per second (scan + tuples in the step)"},
+                       "unit_note": "value = odd candidates per second (scan + tuples in the step; at N>1 the scan phase includes the all-gather of the per-rank counts and lists)"},
                       args.steps * 5)
     line["unit"] = "Gcandidates/s"
     scan_ms = statistics.median(phase["scan"][-args.steps:])

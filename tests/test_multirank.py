@@ -88,3 +88,36 @@ def test_two_rank_pooled_reduction_matches_single():
         np.testing.assert_allclose(pooled, whole.pooled.numpy(), rtol=1e-13)
         assert abs(corr - ref["corr"]) < 1e-11
         assert abs(corr - whole.pooled_correlation()) < 1e-13
+
+
+def _census_worker(rank, world, port, lo, hi, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import coracle
+    from paper_1811_11629_b200.shard import gather_sorted, shard_interval
+    a, b = shard_interval(lo, hi, world, rank)
+    sp, _ = coracle.census(a, b) if b > a else (np.zeros(0, dtype=np.uint32), None)
+    got = gather_sorted(torch.from_numpy(sp.astype(np.int64)))
+    q.put((rank, got.numpy().tolist()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_census_gather_matches_single(world):
+    """Config 5 across ranks: contiguous candidate intervals per rank, counts
+    and lists all-gathered, equal to the single-process census."""
+    from oracle import coracle
+    lo, hi = 2_000_003, 2_600_000
+    want, _ = coracle.census(lo, hi)
+    port = _free_port()
+    q = tmp.get_context("spawn").SimpleQueue()
+    procs = [tmp.get_context("spawn").Process(target=_census_worker, args=(r, world, port, lo, hi, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get() for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert res[r] == want.astype(np.int64).tolist()
