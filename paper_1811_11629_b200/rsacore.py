@@ -263,10 +263,17 @@ def _scalar_run(state: GeneratorState, params: GeneratorParams, count: int, raw:
     out_raw = torch.empty(count, dtype=torch.uint64, device=d) if raw else None
     out_f64 = torch.empty(count, dtype=torch.float64, device=d) if f64 else None
     if count:
-        _lib.call("rsa_fill", inst.data_ptr(), 1, 1, count, params.e, instance_flags(params),
-                  m1.data_ptr(), m2.data_ptr(), s.data_ptr(),
-                  out_raw.data_ptr() if raw else None, out_f64.data_ptr() if f64 else None,
-                  count, _device.stream(d))
+        flags = instance_flags(params)
+        args = (inst.data_ptr(), 1, 1, count, params.e, flags, m1.data_ptr(), m2.data_ptr(), s.data_ptr(),
+                out_raw.data_ptr() if raw else None, out_f64.data_ptr() if f64 else None, count)
+        L = _lib.load()
+        if flags & _lib.RSA_FLAG_FAST and (raw or f64) and int(L.rsa_fill_segments(1, count)) > 1:
+            # one lane, many draws: split it across threads (K1s, bit-identical)
+            nb = int(L.rsa_fill_segmented_scratch_bytes(1, count))
+            scratch = torch.empty(nb, dtype=torch.uint8, device=d)
+            _lib.call("rsa_fill_segmented", *args, scratch.data_ptr(), nb, _device.stream(d))
+        else:
+            _lib.call("rsa_fill", *args, _device.stream(d))
     new = _device.to_ints(st)
     state.m1, state.m2 = new[0], new[1]
     if params.skip_mode == SKIP_LCG or (params.skip_mode == SKIP_UNIT and count):
