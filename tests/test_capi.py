@@ -74,3 +74,18 @@ def test_argument_errors_need_no_gpu():
     assert lib.rsa_fused_stats(None, 3, 1, 9, None, None, None, None, None, None) == _lib.RSA_EINVAL
     assert lib.rsa_safe_prime_scan_scratch_bytes(0, (1 << 32) + 1) == 0
     assert lib.rsa_safe_prime_scan_scratch_bytes(1 << 31, 1 << 32) > 0
+
+
+def test_c_abi_example_compiles(tmp_path):
+    """examples/c_abi_stream0.c (the hot path through the C ABI alone) builds
+    against include/rsarand_b200.h and links against the library."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None or not os.path.exists("/usr/local/cuda/include/cuda_runtime.h"):
+        pytest.skip("gcc / CUDA headers not available")
+    from paper_1811_11629_b200 import _lib
+    libdir = os.path.dirname(_lib.lib_path())
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run(["gcc", "-O2", f"-I{root}/include", "-I/usr/local/cuda/include",
+                    os.path.join(root, "examples", "c_abi_stream0.c"), "-o", str(tmp_path / "ex"),
+                    f"-L{libdir}", "-lrsarand_b200", "-L/usr/local/cuda/lib64", "-lcudart"], check=True)
