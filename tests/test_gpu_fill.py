@@ -353,6 +353,15 @@ def test_capi_argument_errors(p0):
                         None, o.data_ptr(), 0, sp) == _lib.RSA_OK
     with pytest.raises(_lib.RsaCudaError):
         _lib.call("rsa_safe_prime_scan", 0, (1 << 32) + 1, None, 0, st.data_ptr(), None, 0, sp)
+    # the interleaved / low-32 layouts exist on the fast kernel only
+    for extra in (_lib.RSA_FLAG_INTERLEAVE, _lib.RSA_FLAG_LOW32):
+        assert lib.rsa_fill(inst.data_ptr(), 1, 4, 2, 9, _lib.RSA_FLAG_GENERAL_PATH | extra, st.data_ptr(),
+                            st.data_ptr(), st.data_ptr(), None, o.data_ptr(), 8, sp) == _lib.RSA_EPARAMS
+    # segmented fill: no output is an error, a non-fast instance is rejected
+    assert lib.rsa_fill_segmented(inst.data_ptr(), 1, 1, 4096, 9, 1, st.data_ptr(), st.data_ptr(),
+                                  st.data_ptr(), None, None, 4096, st.data_ptr(), 8, sp) == _lib.RSA_EINVAL
+    assert lib.rsa_fill_segmented(inst.data_ptr(), 1, 1, 4096, 9, 0, st.data_ptr(), st.data_ptr(),
+                                  st.data_ptr(), None, o.data_ptr(), 4096, st.data_ptr(), 8, sp) == _lib.RSA_EPARAMS
 
 
 def test_float_map_many_moduli_and_near_midpoints(golden_streams):
