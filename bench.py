@@ -165,17 +165,20 @@ def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    steps = []
+    steps, walls = [], []
     for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
         r = cpu_port_rate(blocks=2)
         if i >= args.warmup:
             steps.append(r)
+            walls.append(time.perf_counter() - t0)
     value = statistics.median([s["value"] for s in steps])
     cb = dict(steps[-1])
     cb["value"] = value
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Gnumbers/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": statistics.median(walls) * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None,
             "dtype": "u64/u32 modular + f64 map", "data": "synthetic (seeded m0, derived params)",
             "config": {"workload": "config2 bulk fill (CPU port sample)", "exponents": list(EXPONENTS),
                        "mv": 65536},
