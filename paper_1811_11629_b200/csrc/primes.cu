@@ -230,6 +230,31 @@ constexpr Wheel cx_wheel() {
 }
 __device__ const Wheel g_wheel = cx_wheel();
 
+#ifndef RSA_WHEEL2
+#define RSA_WHEEL2 1
+#endif
+#if RSA_WHEEL2
+// Second wheel for 17, 19, 23 (period 7429), OR-ed into the first.
+constexpr uint32_t WHEEL2 = 17 * 19 * 23;
+constexpr uint32_t WHEEL2_INV12 = cx_inv_mod(12, WHEEL2);
+constexpr int WHEEL2_WORDS = (int)((WHEEL2 + SCAN_PER_CTA + 3) / 4 + 1);
+struct Wheel2 {
+    uint32_t w[WHEEL2_WORDS];
+};
+constexpr Wheel2 cx_wheel2() {
+    Wheel2 t{};
+    const uint32_t ls[3] = {17, 19, 23};
+    for (uint32_t x = 0; x < 4u * WHEEL2_WORDS; ++x) {
+        const uint32_t v = x % WHEEL2;
+        bool m = false;
+        for (uint32_t l : ls) m = m || v % l == 0 || v % l == WHEEL2_INV12 % l;
+        if (m) t.w[x / 4] |= 1u << (8 * (x % 4));
+    }
+    return t;
+}
+__device__ const Wheel2 g_wheel2 = cx_wheel2();
+#endif
+
 // first u with l | p_u (q = false) or l | q_u (q = true), inv = 12^-1 or 6^-1 mod l
 RSA_DEV uint32_t sieve_start(uint64_t P0, uint32_t l, uint32_t inv, bool q) {
     const uint64_t v = q ? (P0 - 1) >> 1 : P0;
@@ -239,7 +264,7 @@ RSA_DEV uint32_t sieve_start(uint64_t P0, uint32_t l, uint32_t inv, bool q) {
 
 // sieve tiers over c_sieve: [0, 4) the wheel, [4, 16) CTA-cooperative marking,
 // [16, NSIEVE) warp-cooperative, then g_big one entry per thread
-constexpr int TIER_A0 = 4, TIER_B0 = 16;
+constexpr int TIER_A0 = RSA_WHEEL2 ? 7 : 4, TIER_B0 = 16;
 static_assert(2 * (TIER_B0 - TIER_A0) <= SCAN_BLOCK, "tier-A starts: one thread each");
 static_assert(2 * (NSIEVE - TIER_B0) <= 32 * (SCAN_BLOCK / 32), "tier-B entries: <= 32 per warp");
 
@@ -264,12 +289,21 @@ k_scan_sieve(ScanRange R, uint64_t cta0, uint32_t* __restrict__ words, uint32_t*
         for (uint32_t w = threadIdx.x; w < WORDS_PER_CTA; w += SCAN_BLOCK) flags[w] = 0;
     if constexpr (SIEVE) {
         const uint64_t P0 = R.first + 12ull * (base - R.nspec);
-        {   // wheel copy (5, 7, 11, 13)
+        {   // wheel copy (5, 7, 11, 13; and 17, 19, 23)
             const uint32_t t0 = (uint32_t)(P0 % WHEEL) * WHEEL_INV12 % WHEEL;
             const uint32_t a0 = t0 >> 2, sh = (t0 & 3) * 8;
+#if RSA_WHEEL2
+            const uint32_t t1 = (uint32_t)(P0 % WHEEL2) * WHEEL2_INV12 % WHEEL2;
+            const uint32_t b0 = t1 >> 2, sh2 = (t1 & 3) * 8;
+#endif
             uint32_t* c32 = reinterpret_cast<uint32_t*>(comp);
-            for (uint32_t x = threadIdx.x; x < SCAN_PER_CTA / 4; x += SCAN_BLOCK)
-                c32[x] = __funnelshift_r(__ldg(&g_wheel.w[a0 + x]), __ldg(&g_wheel.w[a0 + x + 1]), sh);
+            for (uint32_t x = threadIdx.x; x < SCAN_PER_CTA / 4; x += SCAN_BLOCK) {
+                uint32_t w = __funnelshift_r(__ldg(&g_wheel.w[a0 + x]), __ldg(&g_wheel.w[a0 + x + 1]), sh);
+#if RSA_WHEEL2
+                w |= __funnelshift_r(__ldg(&g_wheel2.w[b0 + x]), __ldg(&g_wheel2.w[b0 + x + 1]), sh2);
+#endif
+                c32[x] = w;
+            }
         }
         if (threadIdx.x < 2 * (TIER_B0 - TIER_A0)) {
             const uint32_t k = 2 * TIER_A0 + threadIdx.x;
