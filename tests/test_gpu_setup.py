@@ -24,7 +24,8 @@ def test_full_census(golden_census):
 
 @pytest.mark.parametrize("lo,hi", [(2, 5000), (0, 12), (5, 8), (11, 12), ((1 << 31) + 1, (1 << 31) + 100_001),
                                    ((1 << 32) - 1_000_000, 1 << 32), (3037000000, 3037100000),
-                                   (1_000_000, 1_200_000)])
+                                   (1_000_000, 1_200_000), (10_000, 400_000), (10_190, 10_230),
+                                   ((1 << 31) - 5, (1 << 31) + 5), (3_000_000_011, 3_000_000_012)])
 def test_scan_windows(lo, hi):
     got = R.safe_primes_in(lo, hi).cpu().numpy().tolist()
     want = [p for p in range(max(lo, 2), min(hi, 11)) if O.is_safe_prime(p)]
