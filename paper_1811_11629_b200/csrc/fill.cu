@@ -136,24 +136,62 @@ __global__ void k_init_lanes(const rsa_instance* __restrict__ inst, uint32_t mv,
                              uint64_t m0_lo, uint64_t m0_hi, uint64_t s0,
                              uint64_t* __restrict__ m1, uint64_t* __restrict__ m2,
                              uint64_t* __restrict__ s) {
-    uint64_t lane = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // a^stride (63-bit exponent) is shared by every lane of an instance: the
+    // first thread computes it for the CTA's first instance
+    __shared__ uint64_t A0, S0;  // a^stride; s0 * A0^(g of the CTA's first lane)
+    __shared__ uint64_t i0;
+    __shared__ uint32_t r1_0, r2_0;  // m0 mod p1, p2 of that instance
+    const uint64_t lane0 = (uint64_t)blockIdx.x * blockDim.x;
+    if (threadIdx.x == 0 && lane0 < total_lanes) {
+        const uint64_t ii = lane0 / mv;
+        const rsa_instance* ip0 = inst + ii;
+        i0 = ii;
+        r1_0 = mod128_32(m0_lo, m0_hi, ip0->p1);
+        r2_0 = mod128_32(m0_lo, m0_hi, ip0->p2);
+        A0 = 0;
+        if (ip0->skip_mode == RSA_SKIP_LCG && ip0->q == Q63) {
+            uint64_t A = 1, b = ip0->a, e = (ip0->q - 1) / mv;
+            while (e) { if (e & 1) A = mulmod_q63(A, b); e >>= 1; if (e) b = mulmod_q63(b, b); }
+            A0 = A;
+            uint64_t t = 1;
+            e = lane0 - ii * mv;  // the first lane's g
+            b = A;
+            while (e) { if (e & 1) t = mulmod_q63(t, b); e >>= 1; if (e) b = mulmod_q63(b, b); }
+            S0 = mulmod_q63(s0 % Q63, t);
+        }
+    }
+    __syncthreads();
+    uint64_t lane = lane0 + threadIdx.x;
     if (lane >= total_lanes) return;
     uint64_t i = lane / mv;
     uint32_t g = (uint32_t)(lane - i * mv);
     const rsa_instance* ip = inst + i;
     uint32_t p1 = ip->p1, p2 = ip->p2;
-    uint32_t r1 = mod128_32(m0_lo, m0_hi, p1), r2 = mod128_32(m0_lo, m0_hi, p2);
+    const uint32_t r1 = i == i0 ? r1_0 : mod128_32(m0_lo, m0_hi, p1);
+    const uint32_t r2 = i == i0 ? r2_0 : mod128_32(m0_lo, m0_hi, p2);
     if (ip->skip_mode == RSA_SKIP_LCG) {
         // lane g: s0 * (a^stride)^g mod q (skipgen.py:124-138)
         uint64_t q = ip->q, stride = (q - 1) / mv;
         uint64_t A, sg;
         if (q == Q63) {
-            A = 1;
-            uint64_t b = ip->a, e = stride;
-            while (e) { if (e & 1) A = mulmod_q63(A, b); e >>= 1; if (e) b = mulmod_q63(b, b); }
-            uint64_t t = 1; b = A; e = g;
-            while (e) { if (e & 1) t = mulmod_q63(t, b); e >>= 1; if (e) b = mulmod_q63(b, b); }
-            sg = mulmod_q63(s0, t);
+            uint64_t b, e;
+            if (i == i0) {  // lane g = g0 + threadIdx.x: s0 A^g0 (shared) times A^threadIdx.x
+                uint64_t t = 1;
+                b = A0;
+                e = threadIdx.x;
+                while (e) { if (e & 1) t = mulmod_q63(t, b); e >>= 1; if (e) b = mulmod_q63(b, b); }
+                sg = mulmod_q63(S0, t);
+            } else {
+                A = 1;
+                b = ip->a;
+                e = stride;
+                while (e) { if (e & 1) A = mulmod_q63(A, b); e >>= 1; if (e) b = mulmod_q63(b, b); }
+                uint64_t t = 1;
+                b = A;
+                e = g;
+                while (e) { if (e & 1) t = mulmod_q63(t, b); e >>= 1; if (e) b = mulmod_q63(b, b); }
+                sg = mulmod_q63(s0, t);
+            }
         } else {
             A = powmod64(ip->a, stride, q);
             sg = mulmod64(s0, powmod64(A, g, q), q);
