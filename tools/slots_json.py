@@ -26,7 +26,7 @@ def count(fn: str) -> float:
 
 res = {}
 for e in (3, 5, 9, 17, 65537):
-    res[f"fill_e{e}"] = count(f"_ZN3rsa11k_fill_fastILj{e}ELi2ELb0ELb1EEEvPK12rsa_instancejmmPmS4_S4_S4_Pdm") / 2
+    res[f"fill_e{e}"] = count(f"_ZN3rsa11k_fill_fastILj{e}ELi2ELb0ELi1EEEvPK12rsa_instancejmmPmS4_S4_S4_Pdmj") / 2
     res[f"fused_e{e}"] = None
 for e in (3, 5, 9, 17):
     try:
