@@ -304,7 +304,7 @@ def run_config2(args, world, rank, local):
     hbm_peak = pk.get("hbm_gbs")
     traffic = load_traffic(f"fill_e{dom}")
     lpt = 1 if args.one_lane else 2
-    roofline = {"bound": "imad", "kernel": f"k_fill_fast<{dom},{lpt},false,true> (e={dom})",
+    roofline = {"bound": "imad", "kernel": f"k_fill_fast<{dom}, {lpt}, 0, 1> (e={dom})",
                 "achieved": imad_ach / 1e12, "peak": peak["ops_per_s"] / 1e12, "unit": "Tops/s",
                 "frac": imad_ach / peak["ops_per_s"], "traffic": traffic,
                 "algorithmic_ops_per_draw": w_imad(dom), "draws_per_launch": count,
