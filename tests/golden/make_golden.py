@@ -15,6 +15,7 @@ Fixtures written (all small; big streams are pinned by sha256 + samples):
   vectors.json     metadata + sha256 digests of the long streams
   census.json      safe-prime census of [2^31, 2^32) (count, sha256, samples)
   derive_all.json  sha256 of the packed tuples for ids [0, 2^20) (+ [0, 65536))
+  snapshot.json    snapshot / params text of the reference for two streams
 """
 
 from __future__ import annotations
@@ -332,6 +333,20 @@ def gen_battery(out):
         reports=[r.record() for r in rep.reports], errors=rep.errors, seconds=round(time.time() - t, 1))
 
 
+def gen_snapshot(out):
+    """The reference's snapshot / params text for stream 0 after 1234 draws,
+    and for a const-mode test stream (rsacore.py:292-417)."""
+    p = pf.derive_stream_params(pf.StreamKey(SEED, 0))
+    st = rsacore.init(p)
+    rsacore.take_raws(st, p, 1234)
+    cases = {"stream0_after_1234": (rsacore.snapshot(st, p).to_text(), rsacore.params_to_text(p))}
+    pc = rsacore.make_params(p.p1, p.p2, 9, p.skip, skip_mode=rsacore.SKIP_CONST, skip_const=12345)
+    sc = rsacore.init(pc)
+    rsacore.take_raws(sc, pc, 7)
+    cases["const_after_7"] = (rsacore.snapshot(sc, pc).to_text(), rsacore.params_to_text(pc))
+    out["snapshot.json"] = {k: {"snapshot": a, "params": b} for k, (a, b) in cases.items()}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-derive-all", action="store_true")
@@ -357,6 +372,8 @@ def main():
         np.savez_compressed(os.path.join(HERE, "bitsource.npz"), **arr)
     if not only or "streamio" in only:
         gen_streamio(out)
+    if not only or "snapshot" in only:
+        gen_snapshot(out)
     if (not only or "census" in only) and not args.skip_census:
         gen_census(out)
     if (not only or "derive_all" in only) and not args.skip_derive_all:
