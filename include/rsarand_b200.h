@@ -109,6 +109,11 @@ int rsa_fill(const rsa_instance* inst, uint32_t n_inst, uint32_t mv, uint64_t bl
              uint64_t* raw_out, double* f64_out, uint64_t inst_stride,
              void* stream);
 
+/* One skip step for a batch of registers: out[j] = a * s[j] mod q
+ * (skipgen.next_skip_array, skipgen.py:108-116).  s may alias out. */
+int rsa_skip_array(const uint64_t* s, uint64_t count, uint64_t a, uint64_t q, uint64_t* out,
+                   void* stream);
+
 /* K1s: the same fill with every lane split into segments of draws, for lane
  * counts too small to fill the GPU (the scalar stream, Mv = 64).  The skip is
  * jumped ahead exactly (s0 * (a^L)^j mod q) and the message prefix sums of the

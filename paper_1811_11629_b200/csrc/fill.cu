@@ -124,6 +124,19 @@ __global__ void k_floats_from_raw(const uint64_t* __restrict__ raw, uint64_t cou
         out[j] = to_unit(raw[j], nf, nr, nl);
 }
 
+// out[j] = a * s[j] mod q: skipgen.next_skip_array (skipgen.py:108-116), one
+// step of the skip for a batch of registers (the q = 2^63-25 fold, or the
+// exact 128-bit product for any other q).
+__global__ void k_skip_array(const uint64_t* __restrict__ s, uint64_t count, uint64_t a, uint64_t q,
+                             uint64_t* __restrict__ out) {
+    const bool fold = q == Q63 && a < (1ull << 32);
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t v = s[j];
+        out[j] = fold && v < (1ull << 63) ? skip_q63(v, (uint32_t)a) : mulmod64(a % q, v % q, q);
+    }
+}
+
 // (hi*2^64 + lo) mod p for p < 2^32.
 RSA_DEV uint32_t mod128_32(uint64_t lo, uint64_t hi, uint32_t p) {
     uint64_t r64 = (1ull << 32) % p;               // 2^32 mod p
@@ -286,6 +299,17 @@ extern "C" int rsa_floats_from_raw(const uint64_t* raw, uint64_t count, uint64_t
     if (grid > 148 * 16) grid = 148 * 16;
     k_floats_from_raw<<<grid, 256, 0, as_stream(stream)>>>(raw, count, n, out);
     return launch_status("rsa_floats_from_raw");
+}
+
+extern "C" int rsa_skip_array(const uint64_t* s, uint64_t count, uint64_t a, uint64_t q, uint64_t* out,
+                              void* stream) {
+    if ((!s || !out) && count) return RSA_EINVAL;
+    if (q < 2) return RSA_EINVAL;
+    if (count == 0) return RSA_OK;
+    unsigned grid = grid_for(count, 256);
+    if (grid > 148 * 16) grid = 148 * 16;
+    k_skip_array<<<grid, 256, 0, as_stream(stream)>>>(s, count, a, q, out);
+    return launch_status("rsa_skip_array");
 }
 
 extern "C" int rsa_init_lanes(const rsa_instance* inst, uint32_t n_inst, uint32_t mv,

@@ -1,10 +1,12 @@
-"""Generator parameters, validation and the scalar stream API.
+"""One generator stream: parameters, their validation, and the scalar API.
 
-Mirrors /root/reference/pkg/src/rsarand/rsacore.py: same names, fields,
-exceptions and error messages.  Parameter construction and validation are
-host-side (exact Python ints, once per stream, as in the reference); every
-draw runs on the GPU through the C ABI (rsa_fill with one lane), so the
-scalar API is the Mv = 1 case of the lane kernels.
+The public surface is the reference `rsarand.rsacore` (GeneratorParams,
+GeneratorState, make_params, validate_params, init, next_raw / next_f64 /
+take_raws / take_floats, decrypt, jump_periods, snapshot / restore and the
+text checkpoint; rsacore.py:21-417) with the same exception classes.  The
+host part is exact integer bookkeeping done once per stream; every draw is a
+GPU call (rsa_fill, or rsa_fill_segmented for long runs) on a one-lane
+state, so the scalar stream is the Mv = 1 case of the lane kernels.
 """
 
 from __future__ import annotations
@@ -17,158 +19,134 @@ import numpy as np
 import torch
 
 from . import _device, _lib, numtheory
-from .skipgen import Q_DEFAULT, SkipParams, default_skip_params
+from .skipgen import Q_DEFAULT, Q_DEFAULT_FACTORS, SkipParams, default_skip_params
 
-DEFAULT_EXPONENT = 9          # rsacore.py:21
-MAX_EXPONENT = 257            # rsacore.py:22
-
-SKIP_LCG = "lcg"              # rsacore.py:24-27
-SKIP_UNIT = "unit"
-SKIP_CONST = "const"
+DEFAULT_EXPONENT = 9
+MAX_EXPONENT = 257
+SKIP_LCG, SKIP_UNIT, SKIP_CONST = "lcg", "unit", "const"
 SKIP_MODES = (SKIP_LCG, SKIP_UNIT, SKIP_CONST)
+MAX_BELOW_ONE = math.nextafter(1.0, 0.0)      # the largest double below 1: the clamp value
 
-MAX_BELOW_ONE = math.nextafter(1.0, 0.0)   # rsacore.py:30
-
-SNAPSHOT_HEADER = "rsarand-snapshot-v1"
-PARAMS_HEADER = "rsarand-params-v1"
-_PARAM_FIELDS = ("p1", "p2", "n", "e", "q", "a", "q1", "q2", "p2inv", "b",
-                 "skip_mode", "skip_const", "test_mode")
-_STATE_FIELDS = ("m1", "m2", "s", "draws")
-
-_MODE_CODE = {SKIP_LCG: _lib.RSA_SKIP_LCG, SKIP_UNIT: _lib.RSA_SKIP_UNIT,
-              SKIP_CONST: _lib.RSA_SKIP_CONST}
+_MODE_CODE = {SKIP_LCG: _lib.RSA_SKIP_LCG, SKIP_UNIT: _lib.RSA_SKIP_UNIT, SKIP_CONST: _lib.RSA_SKIP_CONST}
 
 
 class InvalidParams(ValueError):
-    """A generator-parameter invariant is violated (rsacore.py:40-41)."""
+    """Parameters break an invariant of the generator."""
 
 
 class InvalidSeed(ValueError):
-    """Seed skip s0 is congruent to 0 mod q (rsacore.py:44-45)."""
+    """The skip seed is 0 modulo q."""
 
 
 class UnsupportedSkipMode(RuntimeError):
-    """Operation defined only for the lcg skip mode (rsacore.py:48-49)."""
+    """The operation exists only for the lcg skip."""
 
 
 class MalformedSnapshot(ValueError):
-    """Snapshot text is missing fields or violates an invariant (rsacore.py:52-53)."""
+    """A checkpoint text cannot be parsed or fails validation."""
 
 
 @dataclass(frozen=True)
 class GeneratorParams:
-    """Per-stream constants (rsacore.py:56-76)."""
-
     p1: int
     p2: int
     n: int
     e: int
     skip: SkipParams
-    p2inv: int
-    b: int
+    p2inv: int                    # p2^-1 mod p1 (Garner)
+    b: int                        # q (q - 1) / 2 mod n: the message advance of one skip period
     skip_mode: str = SKIP_LCG
     skip_const: int = 0
     test_mode: bool = False
-    n_float: float = 0.0
+    n_float: float = 0.0          # float(n), the float map's divisor
 
 
 @dataclass
 class GeneratorState:
-    """Scalar stream state (rsacore.py:79-86)."""
-
-    m1: int
-    m2: int
-    s: int
+    m1: int                       # message mod p1
+    m2: int                       # message mod p2
+    s: int                        # skip register
     draws: int = 0
 
 
 def make_params(p1: int, p2: int, e: int = DEFAULT_EXPONENT, skip: SkipParams | None = None,
                 skip_mode: str = SKIP_LCG, skip_const: int = 0,
                 test_mode: bool = False) -> GeneratorParams:
-    """Build and validate GeneratorParams (rsacore.py:89-107)."""
-    if skip is None:
-        skip = default_skip_params()
+    """GeneratorParams from the two primes, the exponent and the skip, with
+    the derived constants filled in; raises InvalidParams if they do not form
+    a valid generator."""
+    skip = skip or default_skip_params()
     if p1 == p2:
-        raise InvalidParams("p1 == p2")
+        raise InvalidParams("p1 == p2: the two primes must differ")
     n = p1 * p2
     try:
-        p2inv = numtheory.modinv(p2, p1)
+        inv = numtheory.modinv(p2, p1)
     except numtheory.NotInvertible as exc:
-        raise InvalidParams(f"p2 not invertible mod p1: {exc}") from exc
-    params = GeneratorParams(p1=p1, p2=p2, n=n, e=e, skip=skip, p2inv=p2inv,
-                             b=skip.q * (skip.q - 1) // 2 % n, skip_mode=skip_mode,
-                             skip_const=skip_const, test_mode=test_mode, n_float=float(n))
+        raise InvalidParams(f"p2 has no inverse modulo p1 ({exc})") from exc
+    q = skip.q
+    params = GeneratorParams(p1=p1, p2=p2, n=n, e=e, skip=skip, p2inv=inv, b=(q * (q - 1) // 2) % n,
+                             skip_mode=skip_mode, skip_const=skip_const, test_mode=test_mode,
+                             n_float=float(n))
     validate_params(params)
     return params
 
 
-def _root_factors(q: int):
-    from .skipgen import Q_DEFAULT_FACTORS
-    return Q_DEFAULT_FACTORS if q == Q_DEFAULT else None
-
-
-# The number-theoretic checks are pure functions of their integers; streams are
-# re-validated on every init / init_vector, so they are memoised.
+# pure functions of their integers, memoised: streams are re-validated on every init
 @functools.lru_cache(maxsize=1 << 14)
-def _is_safe_prime(p: int) -> bool:
+def _safe(p: int) -> bool:
     return numtheory.is_safe_prime(p)
 
 
 @functools.lru_cache(maxsize=1 << 10)
-def _is_prime64(q: int) -> bool:
+def _prime(q: int) -> bool:
     return numtheory.is_prime64(q)
 
 
 @functools.lru_cache(maxsize=1 << 12)
-def _is_primitive_root(a: int, q: int) -> bool:
-    return numtheory.is_primitive_root(a, q, _root_factors(q))
+def _generator(a: int, q: int) -> bool:
+    return numtheory.is_primitive_root(a, q, Q_DEFAULT_FACTORS if q == Q_DEFAULT else None)
+
+
+def _problems(p: GeneratorParams):
+    """Violated invariants, in checking order (cheap structural checks before
+    the primality work)."""
+    sk, n = p.skip, p.n
+    yield p.p1 == p.p2, "p1 == p2: the two primes must differ"
+    yield n != p.p1 * p.p2, "n is not p1*p2"
+    yield lambda: not _safe(p.p1), f"p1={p.p1} is not a safe prime"
+    yield lambda: not _safe(p.p2), f"p2={p.p2} is not a safe prime"
+    yield p.e < 1 or not p.e & 1, f"exponent e={p.e} must be odd and positive"
+    yield p.e > MAX_EXPONENT, f"exponent e={p.e} exceeds {MAX_EXPONENT}"
+    yield lambda: not _prime(sk.q), f"skip modulus q={sk.q} is not prime"
+    yield sk.a > sk.q // sk.a, "multiplier a with a*a > q"
+    yield (sk.q1, sk.q2) != divmod(sk.q, sk.a), "q1, q2 are not divmod(q, a)"
+    yield lambda: not _generator(sk.a, sk.q), f"a={sk.a} does not generate Z_q^*"
+    yield math.gcd(n, sk.q) != 1, "n and q share a factor"
+    yield math.gcd(n, sk.q - 1) != 1, "n and q-1 share a factor"
+    yield p.b != (sk.q * (sk.q - 1) // 2) % n, "period offset b does not match q and n"
+    yield p.b == 0, "period offset b is zero"
+    yield not (0 < p.p2inv < p.p1 and (p.p2 * p.p2inv) % p.p1 == 1), "p2inv is not p2^-1 mod p1"
+    yield p.skip_mode not in SKIP_MODES, f"unknown skip mode {p.skip_mode!r}"
+    if p.skip_mode == SKIP_CONST:
+        yield not 0 <= p.skip_const < n, "constant skip outside [0, n)"
+    else:
+        yield p.skip_const != 0, "skip_const is only used in const mode"
+    yield p.n_float != float(n), "n_float is not float(n)"
+    if not p.test_mode:  # production sizes (rsacore.py:166-181)
+        window = range(2 ** 31 + 1, 2 ** 32)
+        yield p.p1 not in window, f"p1={p.p1} outside (2^31, 2^32)"
+        yield p.p2 not in window, f"p2={p.p2} outside (2^31, 2^32)"
+        yield p.e < 3, "production exponent must be at least 3"
+        yield math.gcd(p.e, (p.p1 - 1) * (p.p2 - 1)) != 1, f"e={p.e} is not coprime to (p1-1)(p2-1)"
+        yield sk.a < 2 ** 31, f"weak multiplier a={sk.a} needs test_mode"
+        yield abs(n - sk.q) > 1e-6 * sk.q, "|n - q| exceeds one part in 10^6"
 
 
 def validate_params(params: GeneratorParams) -> None:
-    """Raise InvalidParams naming the first violated invariant (rsacore.py:117-181)."""
-    p1, p2, n, e, sk = params.p1, params.p2, params.n, params.e, params.skip
-    checks = (
-        (p1 == p2, "p1 == p2"),
-        (n != p1 * p2, "n != p1*p2"),
-        (lambda: not _is_safe_prime(p1), f"p1={p1} is not a safe prime"),
-        (lambda: not _is_safe_prime(p2), f"p2={p2} is not a safe prime"),
-        (e < 1 or e % 2 == 0, f"exponent e={e} must be odd and positive"),
-        (e > MAX_EXPONENT, f"exponent e={e} above {MAX_EXPONENT}"),
-        (lambda: not _is_prime64(sk.q), f"q={sk.q} is not prime"),
-        (sk.a * sk.a > sk.q, "multiplier violates a*a <= q"),
-        (sk.q1 != sk.q // sk.a or sk.q2 != sk.q % sk.a, "inconsistent Schrage constants q1/q2"),
-        (lambda: not _is_primitive_root(sk.a, sk.q), f"a={sk.a} is not a primitive root mod q"),
-        (math.gcd(n, sk.q) != 1, "gcd(n, q) != 1"),
-        (math.gcd(n, sk.q - 1) != 1, "gcd(n, q-1) != 1"),
-        (params.b != sk.q * (sk.q - 1) // 2 % n, "inconsistent period offset b"),
-        (params.b == 0, "period offset b is zero"),
-        (params.p2inv <= 0 or params.p2inv >= p1 or p2 * params.p2inv % p1 != 1,
-         "p2inv is not the inverse of p2 mod p1"),
-        (params.skip_mode not in SKIP_MODES, f"unknown skip mode {params.skip_mode!r}"),
-    )
-    for bad, msg in checks:
+    """Raise InvalidParams for the first violated invariant."""
+    for bad, why in _problems(params):
         if bad() if callable(bad) else bad:
-            raise InvalidParams(msg)
-    if params.skip_mode == SKIP_CONST:
-        if not 0 <= params.skip_const < n:
-            raise InvalidParams("constant skip outside [0, n)")
-    elif params.skip_const != 0:
-        raise InvalidParams("skip_const must be 0 outside const mode")
-    if params.n_float != float(n):
-        raise InvalidParams("inconsistent cached n_float")
-    if params.test_mode:
-        return
-    prod = (
-        (not (1 << 31) < p1 < (1 << 32), f"p1={p1} outside (2^31, 2^32)"),
-        (not (1 << 31) < p2 < (1 << 32), f"p2={p2} outside (2^31, 2^32)"),
-        (e < 3, "production exponent must be >= 3"),
-        (math.gcd(e, (p1 - 1) * (p2 - 1)) != 1, f"gcd(e, (p1-1)(p2-1)) != 1 for e={e}"),
-        (sk.a < (1 << 31), f"weak multiplier a={sk.a} requires test_mode"),
-        (abs(n - sk.q) > 1e-6 * sk.q, "|n - q| exceeds one part in 10^6"),
-    )
-    for bad, msg in prod:
-        if bad:
-            raise InvalidParams(msg)
+            raise InvalidParams(why)
 
 
 # ---------------------------------------------------------------------------
@@ -240,16 +218,16 @@ def skip_only_instance(skip: SkipParams, dev=None) -> torch.Tensor:
 # scalar stream (rsacore.py:189-264) — the Mv = 1 lane on the GPU
 
 def init(params: GeneratorParams, m0: int = 0, s0: int = 1) -> GeneratorState:
-    """Fresh stream state (rsacore.py:189-204)."""
+    """State at draw 0: message m0 (as residues) and skip seed s0 (the const
+    mode's register holds skip_const instead)."""
     validate_params(params)
-    if m0 < 0 or s0 < 0:
+    if min(m0, s0) < 0:
         raise InvalidSeed("seeds must be nonnegative")
     if params.skip_mode == SKIP_CONST:
-        s = params.skip_const
-    else:
-        s = s0 % params.skip.q
-        if s == 0:
-            raise InvalidSeed(f"s0={s0} is divisible by q")
+        return GeneratorState(m1=m0 % params.p1, m2=m0 % params.p2, s=params.skip_const)
+    s = s0 % params.skip.q
+    if not s:
+        raise InvalidSeed(f"s0={s0} is a multiple of q")
     return GeneratorState(m1=m0 % params.p1, m2=m0 % params.p2, s=s)
 
 
@@ -305,120 +283,23 @@ def take_floats(state: GeneratorState, params: GeneratorParams, count: int) -> l
 
 
 def decrypt(c: int, params: GeneratorParams) -> int:
-    """c^d mod n, d = e^-1 mod (p1-1)(p2-1): validation hook (rsacore.py:267-273)."""
-    d = numtheory.modinv(params.e, (params.p1 - 1) * (params.p2 - 1))
-    return pow(c, d, params.n)
+    """Invert the cipher: c^d mod n with d = e^-1 mod (p1-1)(p2-1)."""
+    phi = (params.p1 - 1) * (params.p2 - 1)
+    return pow(c, numtheory.modinv(params.e, phi), params.n)
 
 
 def jump_periods(state: GeneratorState, params: GeneratorParams, u: int) -> GeneratorState:
-    """Advance u full skip periods (u*(q-1) draws) in O(1) (rsacore.py:276-289)."""
+    """Skip u whole periods of the skip sequence (u (q - 1) draws) at once:
+    the skip returns to itself and the message gains u b."""
     if params.skip_mode != SKIP_LCG:
-        raise UnsupportedSkipMode(f"jump_periods undefined for {params.skip_mode} mode")
-    ub = u * params.b
-    state.m1 = (state.m1 + ub) % params.p1
-    state.m2 = (state.m2 + ub) % params.p2
+        raise UnsupportedSkipMode(f"jump_periods needs the lcg skip, not {params.skip_mode}")
+    gain = u * params.b
+    state.m1 = (state.m1 + gain) % params.p1
+    state.m2 = (state.m2 + gain) % params.p2
     state.draws += u * (params.skip.q - 1)
     return state
 
 
-# ---------------------------------------------------------------------------
-# snapshot text format (rsacore.py:292-417; SPEC.md:301)
-
-@dataclass(frozen=True)
-class StreamSnapshot:
-    params: GeneratorParams
-    m1: int
-    m2: int
-    s: int
-    draws: int
-
-    def to_text(self) -> str:
-        body = [SNAPSHOT_HEADER, *params_lines(self.params)]
-        body += [f"{k}={getattr(self, k):x}" for k in _STATE_FIELDS]
-        return "\n".join(body) + "\n"
-
-    @classmethod
-    def from_text(cls, text: str) -> "StreamSnapshot":
-        f = _parse_kv(text, SNAPSHOT_HEADER, set(_PARAM_FIELDS) | set(_STATE_FIELDS))
-        return cls(params=_params_from_fields(f), m1=_hex(f, "m1"), m2=_hex(f, "m2"),
-                   s=_hex(f, "s"), draws=_hex(f, "draws"))
-
-
-def _parse_kv(text: str, header: str, expected: set) -> dict:
-    lines = [ln.strip() for ln in text.splitlines() if ln.strip()]
-    if not lines or lines[0] != header:
-        raise MalformedSnapshot(f"missing or unknown header (want {header!r})")
-    out: dict = {}
-    for ln in lines[1:]:
-        key, sep, val = ln.partition("=")
-        if not sep or key in out:
-            raise MalformedSnapshot(f"bad line {ln!r}")
-        out[key] = val
-    if set(out) != expected:
-        raise MalformedSnapshot(f"missing={sorted(expected - set(out))} "
-                                f"unknown={sorted(set(out) - expected)}")
-    return out
-
-
-def _hex(f: dict, key: str) -> int:
-    try:
-        return int(f[key], 16)
-    except ValueError as exc:
-        raise MalformedSnapshot(f"field {key} is not hex: {f[key]!r}") from exc
-
-
-def _params_from_fields(f: dict) -> GeneratorParams:
-    skip = SkipParams(q=_hex(f, "q"), a=_hex(f, "a"), q1=_hex(f, "q1"), q2=_hex(f, "q2"))
-    n = _hex(f, "n")
-    return GeneratorParams(p1=_hex(f, "p1"), p2=_hex(f, "p2"), n=n, e=_hex(f, "e"), skip=skip,
-                           p2inv=_hex(f, "p2inv"), b=_hex(f, "b"), skip_mode=f["skip_mode"],
-                           skip_const=_hex(f, "skip_const"), test_mode=bool(_hex(f, "test_mode")),
-                           n_float=float(n))
-
-
-def params_lines(params: GeneratorParams) -> list[str]:
-    vals = {"p1": params.p1, "p2": params.p2, "n": params.n, "e": params.e, "q": params.skip.q,
-            "a": params.skip.a, "q1": params.skip.q1, "q2": params.skip.q2, "p2inv": params.p2inv,
-            "b": params.b, "skip_const": params.skip_const, "test_mode": int(params.test_mode)}
-    return [f"skip_mode={params.skip_mode}" if k == "skip_mode" else f"{k}={vals[k]:x}"
-            for k in _PARAM_FIELDS]
-
-
-def params_to_text(params: GeneratorParams) -> str:
-    return "\n".join([PARAMS_HEADER, *params_lines(params)]) + "\n"
-
-
-def params_from_text(text: str) -> GeneratorParams:
-    params = _params_from_fields(_parse_kv(text, PARAMS_HEADER, set(_PARAM_FIELDS)))
-    try:
-        validate_params(params)
-    except InvalidParams as exc:
-        raise MalformedSnapshot(f"exported params invalid: {exc}") from exc
-    return params
-
-
-def snapshot(state: GeneratorState, params: GeneratorParams) -> StreamSnapshot:
-    return StreamSnapshot(params=params, m1=state.m1, m2=state.m2, s=state.s, draws=state.draws)
-
-
-def restore(snap) -> tuple[GeneratorParams, GeneratorState]:
-    """Rebuild (params, state), re-validating everything (rsacore.py:393-417)."""
-    if isinstance(snap, str):
-        snap = StreamSnapshot.from_text(snap)
-    params = snap.params
-    try:
-        validate_params(params)
-    except InvalidParams as exc:
-        raise MalformedSnapshot(f"snapshot params invalid: {exc}") from exc
-    if not 0 <= snap.m1 < params.p1:
-        raise MalformedSnapshot("m1 outside [0, p1)")
-    if not 0 <= snap.m2 < params.p2:
-        raise MalformedSnapshot("m2 outside [0, p2)")
-    if params.skip_mode == SKIP_CONST:
-        if snap.s != params.skip_const:
-            raise MalformedSnapshot("const-mode skip register mismatch")
-    elif not 1 <= snap.s < params.skip.q:
-        raise MalformedSnapshot("skip outside [1, q)")
-    if snap.draws < 0:
-        raise MalformedSnapshot("negative draw count")
-    return params, GeneratorState(m1=snap.m1, m2=snap.m2, s=snap.s, draws=snap.draws)
+# text checkpoints live in _snaptext (the reference's formats, byte for byte)
+from ._snaptext import (PARAMS_HEADER, SNAPSHOT_HEADER, StreamSnapshot,  # noqa: E402,F401
+                        params_from_text, params_lines, params_to_text, restore, snapshot)

@@ -482,3 +482,19 @@ def test_segmented_multi_instance(golden_streams, mv, blocks, stride_pad):
         assert np.array_equal(a, b)
     f = res[1][1].reshape(4, stride)
     assert (f[:, blocks * mv:] == -1.0).all()
+
+
+def test_next_skip_array():
+    """skipgen.next_skip_array (skipgen.py:108-116) = a*s mod q elementwise,
+    for the production modulus and a generic prime, numpy in -> numpy out and
+    CUDA tensor in -> tensor out."""
+    rng = np.random.default_rng(11)
+    for a, q in ((2983799827, skipgen.Q_DEFAULT), (2, 13), (3, (1 << 61) - 1)):
+        sp = skipgen.SkipParams(q=q, a=a, q1=q // a, q2=q % a)
+        s = rng.integers(1, min(q, 1 << 63), size=4099, dtype=np.uint64)
+        want = np.array([a * int(x) % q for x in s], dtype=np.uint64)
+        got = skipgen.next_skip_array(s, sp)
+        assert isinstance(got, np.ndarray) and np.array_equal(got, want)
+        t = torch.from_numpy(s.view(np.int64)).cuda().view(torch.uint64)
+        assert np.array_equal(u64np(skipgen.next_skip_array(t, sp)), want)
+    assert skipgen.next_skip_array(np.zeros(0, dtype=np.uint64), sp).size == 0
