@@ -1,13 +1,13 @@
-"""Deterministic per-stream parameters — the drop-in for rsarand.paramfactory.
+"""Per-stream parameters from (master seed, stream id) — drop-in for
+`rsarand.paramfactory` (same names, constants and exceptions;
+paramfactory.py:24-278).
 
-Mirrors /root/reference/pkg/src/rsarand/paramfactory.py (constants, StreamKey,
-safe_primes_in, nth_safe_prime_in, find_pair, stream_indices,
-derive_stream_params, exceptions).  The reference's lazily sieved p1 table
-(paramfactory.py:160-189) becomes one device-resident list of all 3,060,794
-safe primes in [2^31, 2^32), built once per device by the K3 Miller-Rabin scan
-(csrc/primes.cu); pair search and instance construction run in K4
-(csrc/setup.cu), one thread per stream id.  `derive_params_table` is the batch
-form the many-instance and fused configurations use.
+Where the reference sieves the p1 window lazily and searches partners with
+per-candidate Miller-Rabin calls, this module keeps ONE device-resident sorted
+list of all 3,060,794 safe primes of [2^31, 2^32) (built once per device by
+the K3 scan, csrc/primes.cu) plus its 2^16-bucket index; the pair search and
+the instance constants run in K4 (csrc/setup.cu), one thread per stream id.
+`derive_params_table` is the batch form (configs 3-5).
 """
 
 from __future__ import annotations
@@ -23,27 +23,27 @@ import torch
 from . import _device, _lib, numtheory, rsacore
 from .skipgen import MULTIPLIER_TABLE, Q_DEFAULT, SkipParams
 
-DEFAULT_MASTER_SEED = 0x243F6A8885A308D3   # paramfactory.py:24
-DEFAULT_TOLERANCE = 1e-6                   # paramfactory.py:25
-SQRT_Q = 3037000499                        # paramfactory.py:27
-P1_WINDOW = ((1 << 31) + 1, SQRT_Q + 1)    # paramfactory.py:30
-N_P1_WINDOW = 1_291_847                    # paramfactory.py:35-36
-N_P2_WINDOW = 1_768_947
-K_P1 = 1_291_831                           # paramfactory.py:41-42
-K_P2 = 1_768_937
-SIGMA = 35_705_744_587                     # paramfactory.py:47-48
-EPSILON = 7
-MAX_STEPS = 256                            # paramfactory.py:270
+# published constants of the reference (paramfactory.py:24-48, 270)
+DEFAULT_MASTER_SEED = 0x243F6A8885A308D3   # the hex digits of pi
+DEFAULT_TOLERANCE = 1e-6                   # |p1 p2 - q| <= tolerance * q
+SQRT_Q = math.isqrt(Q_DEFAULT)             # 3037000499
+P1_WINDOW = (2 ** 31 + 1, SQRT_Q + 1)      # p1 in (2^31, sqrt(q)], p2 above it
+N_P1_WINDOW = 1_291_847                    # safe primes in the p1 window
+N_P2_WINDOW = 1_768_947                    # ... and in (sqrt(q), 2^32)
+K_P1, K_P2 = 1_291_831, 1_768_937          # prime radices of the index space (<= the window counts)
+SIGMA = 35_705_744_587                     # stream-id stride, coprime to the index space
+EPSILON = 7                                # the index permutation x -> x^7 mod S
+MAX_STEPS = 256                            # bounded ordinal advance
 
-SAFE_PRIME_CENSUS = 3_060_794              # [2^31, 2^32) (test_acceptance.py:152-153)
+SAFE_PRIME_CENSUS = 3_060_794              # safe primes in [2^31, 2^32) (test_acceptance.py:152-153)
 
 
 class NotFound(LookupError):
-    """No qualifying safe prime in the requested range/window (paramfactory.py:51-52)."""
+    """The requested safe prime or partner does not exist in the range."""
 
 
 class DerivationExhausted(RuntimeError):
-    """No valid parameter set within the bounded ordinal advance (paramfactory.py:55-56)."""
+    """MAX_STEPS ordinal advances found no valid prime pair."""
 
 
 @dataclass(frozen=True)
@@ -90,21 +90,21 @@ def safe_primes_in(lo: int, hi: int, dev=None) -> torch.Tensor:
 
 
 def nth_safe_prime_in(lo: int, hi: int, k: int, dev=None) -> int:
-    """The k-th (0-based) safe prime >= lo, below hi (paramfactory.py:133-157)."""
-    if lo >= hi:
-        raise ValueError("empty range")
+    """The safe prime of ordinal k (0-based) among those in [lo, hi)."""
+    if hi <= lo:
+        raise ValueError("empty range: need lo < hi")
     if k < 0:
         raise ValueError("ordinal must be >= 0")
-    if hi > 1 << 32:
+    if hi > 2 ** 32:
         raise NotImplementedError("the device scan covers [0, 2^32)")
-    # widen in 2^24 segments like the reference, scanning only what is needed
-    seen = 0
-    for start in range(lo, hi, 1 << 24):
-        arr = safe_primes_u32(start, min(start + (1 << 24), hi), dev)
-        if seen + arr.numel() > k:
-            return int(arr[k - seen].item())
-        seen += arr.numel()
-    raise NotFound(f"fewer than {k + 1} safe primes in [{lo}, {hi})")
+    step = 1 << 24      # scan only as far as the ordinal needs
+    before = 0
+    for a in range(lo, hi, step):
+        chunk = safe_primes_u32(a, min(a + step, hi), dev)
+        if k < before + chunk.numel():
+            return int(chunk[k - before].item())
+        before += chunk.numel()
+    raise NotFound(f"only {before} safe primes in [{lo}, {hi}), no ordinal {k}")
 
 
 def safe_prime_index(sp: torch.Tensor) -> torch.Tensor:
@@ -165,51 +165,60 @@ def tolerance_int(tol: float, q: int) -> int:
 
 
 def find_pair(p1: int, q: int = Q_DEFAULT, tol: float = DEFAULT_TOLERANCE, dev=None) -> tuple[int, int]:
-    """(p1, p2): the safe prime nearest floor(q/p1), ties to the smaller, p2 != p1,
-    2^31 < p2 < 2^32, |p1 p2 - q| <= tol q (paramfactory.py:195-219)."""
-    if not (1 << 31) < p1 < (1 << 32) or not numtheory.is_safe_prime(p1):
+    """(p1, p2) with p2 the 32-bit safe prime closest to floor(q / p1) (the
+    smaller on a tie), p2 != p1 and |p1 p2 - q| <= tol q."""
+    if p1 <= 2 ** 31 or p1 >= 2 ** 32 or not numtheory.is_safe_prime(p1):
         raise ValueError(f"p1={p1} is not a 32-bit safe prime")
-    t = tolerance_int(tol, q)
-    if t < 0:
-        raise NotFound(f"no safe-prime partner for p1={p1} within {tol} of q")
-    if not 0 < q < 1 << 64:
+    if not 0 < q < 2 ** 64:
         raise NotImplementedError("q must fit in 64 bits")
+    limit = tolerance_int(tol, q)
+    missing = NotFound(f"no safe prime p2 with |p1*p2 - q| <= {tol}*q for p1={p1}")
+    if limit < 0:
+        raise missing
     tab = safe_prime_table(dev)
     d = tab.device
-    p1t = torch.tensor([p1], dtype=torch.int64, device=d).to(torch.uint32)
-    p2 = torch.zeros(1, dtype=torch.uint32, device=d)
-    st = torch.zeros(1, dtype=torch.int32, device=d)
-    _lib.call("rsa_find_pair", p1t.data_ptr(), 1, q, min(t, (1 << 64) - 1), tab.sp.data_ptr(),
-              tab.n_sp, tab.index.data_ptr(), p2.data_ptr(), st.data_ptr(), _device.stream(d))
-    if int(st.item()) != 0:
-        raise NotFound(f"no safe-prime partner for p1={p1} within {tol} of q")
-    return p1, int(p2.to(torch.int64).item())
+    p1_dev = torch.tensor([p1], dtype=torch.int64, device=d).to(torch.uint32)
+    p2_dev = torch.zeros(1, dtype=torch.uint32, device=d)
+    status = torch.zeros(1, dtype=torch.int32, device=d)
+    _lib.call("rsa_find_pair", p1_dev.data_ptr(), 1, q, min(limit, 2 ** 64 - 1), tab.sp.data_ptr(),
+              tab.n_sp, tab.index.data_ptr(), p2_dev.data_ptr(), status.data_ptr(), _device.stream(d))
+    if int(status.item()):
+        raise missing
+    return p1, int(p2_dev.to(torch.int64).item())
 
 
 # ---------------------------------------------------------------------------
 # derivation
 
+def _phi(n: int) -> int:
+    phi = n
+    for p in numtheory.factor64(n).distinct_primes():
+        phi = phi // p * (p - 1)
+    return phi
+
+
 @functools.lru_cache(maxsize=8)
 def _index_space(n_a: int) -> int:
-    """K_P1*K_P2*n_a, with the published constants re-checked (paramfactory.py:225-239)."""
-    space = K_P1 * K_P2 * n_a
-    if not numtheory.is_prime64(K_P1) or not numtheory.is_prime64(K_P2):
-        raise RuntimeError("index radices must be prime")
-    if math.gcd(SIGMA, space) != 1:
-        raise RuntimeError("SIGMA shares a factor with the index space")
-    phi = 1
-    for p, k in numtheory.factor64(space).factors:
-        phi *= (p - 1) * p ** (k - 1)
-    if math.gcd(EPSILON, phi) != 1:
-        raise RuntimeError("EPSILON shares a factor with phi(index space)")
-    return space
+    """S = K_P1 K_P2 n_a, after checking that id -> (t + id SIGMA)^EPSILON
+    mod S is a permutation: SIGMA a unit and EPSILON coprime to phi(S)."""
+    S = K_P1 * K_P2 * n_a
+    radices_prime = numtheory.is_prime64(K_P1) and numtheory.is_prime64(K_P2)
+    if not radices_prime:
+        raise RuntimeError("K_P1 and K_P2 must be prime")
+    if math.gcd(S, SIGMA) > 1:
+        raise RuntimeError(f"SIGMA is not a unit modulo the index space {S}")
+    if math.gcd(_phi(S), EPSILON) > 1:
+        raise RuntimeError(f"x -> x^{EPSILON} does not permute Z_{S}")
+    return S
 
 
 def stream_indices(key: StreamKey, n_a: int = len(MULTIPLIER_TABLE)) -> tuple[int, int]:
-    """(p1 ordinal, multiplier index) (paramfactory.py:242-250); host scalar, exact."""
-    space = _index_space(n_a)
-    beta = pow((key.master_seed + key.stream_id * SIGMA) % space, EPSILON, space)
-    return beta % K_P1, beta // (K_P1 * K_P2) % n_a
+    """(p1 ordinal, multiplier index) of a stream: beta = (t + id SIGMA)^EPSILON
+    mod S, ordinal = beta mod K_P1, index = floor(beta / (K_P1 K_P2)) mod n_a."""
+    S = _index_space(n_a)
+    beta = pow((key.master_seed + key.stream_id * SIGMA) % S, EPSILON, S)
+    upper, ordinal = divmod(beta, K_P1)
+    return ordinal, (upper // K_P2) % n_a
 
 
 @functools.lru_cache(maxsize=64)
@@ -318,30 +327,29 @@ def derive_stream_params(key: StreamKey, e: int = rsacore.DEFAULT_EXPONENT,
                          multiplier_table: tuple = MULTIPLIER_TABLE,
                          skip_mode: str = rsacore.SKIP_LCG, skip_const: int = 0,
                          multiplier: int | None = None, dev=None) -> rsacore.GeneratorParams:
-    """GeneratorParams for a stream key (paramfactory.py:253-278): the device
-    search picks (p1, p2); the host re-validates with make_params and, should it
-    reject the pair, resumes the search at the next ordinal step."""
-    if not multiplier_table:
+    """GeneratorParams of one stream.  The device picks (p1, p2) from the
+    stream's ordinal (advancing at most MAX_STEPS ordinals); the host then
+    builds and validates the params with make_params and, if that rejects the
+    pair, resumes the device search one ordinal further."""
+    if len(multiplier_table) == 0:
         raise ValueError("multiplier table must be non-empty")
-    ordinal, a_index = stream_indices(key, len(multiplier_table))
-    a = multiplier if multiplier is not None else multiplier_table[a_index]
-    skip = SkipParams.create(a)
-    if not _exponent_usable(e) or key.stream_id < 0 or key.master_seed < 0:
-        raise DerivationExhausted(f"no valid parameters near ordinal {ordinal}")
-    start = 0
-    while start < MAX_STEPS:
-        cfg = _setup_config(key.master_seed, key.stream_id % (1 << 64), e, len(multiplier_table),
-                            a, start)
-        # stream_id enters only through id*SIGMA mod S, so reduce it mod S exactly
-        cfg.first_id = key.stream_id % _index_space(len(multiplier_table))
-        t = _run_setup(cfg, 1, tuple(multiplier_table), dev)
-        if int(t.status[0].item()) != 0:
+    n_a = len(multiplier_table)
+    ordinal, a_index = stream_indices(key, n_a)
+    skip = SkipParams.create(multiplier_table[a_index] if multiplier is None else multiplier)
+    exhausted = DerivationExhausted(f"no valid parameters within {MAX_STEPS} ordinals of {ordinal}")
+    if min(key.stream_id, key.master_seed) < 0 or not _exponent_usable(e):
+        raise exhausted
+    step = 0
+    while step < MAX_STEPS:
+        cfg = _setup_config(key.master_seed, 0, e, n_a, skip.a, step)
+        cfg.first_id = key.stream_id % _index_space(n_a)   # ids enter only through id*SIGMA mod S
+        found = _run_setup(cfg, 1, tuple(multiplier_table), dev)
+        if int(found.status[0].item()):
             break
-        rec = t.records()[0]
-        step = int(t.steps[0].item())
+        rec = found.records()[0]
         try:
             return rsacore.make_params(int(rec["p1"]), int(rec["p2"]), e, skip,
                                        skip_mode=skip_mode, skip_const=skip_const)
         except rsacore.InvalidParams:
-            start = step + 1
-    raise DerivationExhausted(f"no valid parameters near ordinal {ordinal}")
+            step = int(found.steps[0].item()) + 1
+    raise exhausted
