@@ -88,3 +88,12 @@ def test_weakened_modes():
     unit1 = rsacore.make_params(p.p1, p.p2, 1, p.skip, skip_mode=rsacore.SKIP_UNIT, test_mode=True)
     weak = stats.run_battery(factory(unit1), budget=10_000_000, tests=["frequency", "serial_d2", "max_of_t"])
     assert not weak.all_pass
+
+
+def test_calibration_sources():
+    """stats.UniformSource passes, stats.ArraySource of a constant fails
+    (the reference's calibration helpers, stats.py:138-160)."""
+    assert stats.freq_test(stats.UniformSource(9), 1 << 21).pass_1e6
+    assert not stats.freq_test(stats.ArraySource([0.25]), 1 << 21).pass_1e6
+    src = stats.ArraySource([0.1, 0.2, 0.3])
+    assert src.take(4).tolist() == [0.1, 0.2, 0.3, 0.1] and src.take(2).tolist() == [0.2, 0.3]
