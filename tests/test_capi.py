@@ -89,3 +89,23 @@ def test_c_abi_example_compiles(tmp_path):
     subprocess.run(["gcc", "-O2", f"-I{root}/include", "-I/usr/local/cuda/include",
                     os.path.join(root, "examples", "c_abi_stream0.c"), "-o", str(tmp_path / "ex"),
                     f"-L{libdir}", "-lrsarand_b200", "-L/usr/local/cuda/lib64", "-lcudart"], check=True)
+
+
+def test_no_cpu_fallback(monkeypatch):
+    """The product path never computes on the host: without a CUDA device
+    every draw / scan entry point raises RsaCudaError, and a missing library
+    is an error rather than a fallback."""
+    import torch
+    import paper_1811_11629_b200 as R
+    if torch.cuda.is_available():
+        pytest.skip("needs a host without a GPU")
+    p = R.make_params(2663418827, 3462982283, 9, R.SkipParams.create(2983799827))
+    for call in (lambda: R.init_vector(p, mv=4), lambda: R.rsacore.take_raws(R.init(p), p, 4),
+                 lambda: R.safe_primes_in(11, 1000),
+                 lambda: R.derive_stream_params(R.StreamKey(R.DEFAULT_MASTER_SEED, 0))):
+        with pytest.raises(_lib.RsaCudaError):
+            call()
+    monkeypatch.setenv("RSARAND_B200_LIB", "/nonexistent/librsarand_b200.so")
+    monkeypatch.setattr(_lib, "_LIB", None)
+    with pytest.raises(_lib.RsaCudaError):
+        _lib.load(build_if_missing=False)
