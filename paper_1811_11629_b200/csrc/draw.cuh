@@ -16,8 +16,32 @@ namespace rsa {
 // (q = 2^63-25, p1, p2 in (2^31, 2^32), lcg skip).
 struct FastInst {
     uint32_t p1, p2, p1_inv, p2_inv, a, k1, k2, garner, r2_1, r2_2, e;
+    uint32_t gA, gB;  // fused-Garner constants (draw_fast_hc<E, true>)
     double p2d, n_float, n_recip, n_recip_lo;
 };
+
+// Fused Garner (p1's k-correction folded into the Garner product): valid when
+// 2 (p1-1)^2 < 2^64, i.e. p1 <= floor(sqrt(q)) — every derived stream
+// (paramfactory.py:27-30 puts p1 in (2^31, floor(sqrt q)]).  Instances with a
+// larger p1 (make_params with the primes given in the other order) take the
+// two-product form.
+#ifndef RSA_GARNER_FUSED
+#define RSA_GARNER_FUSED 1
+#endif
+constexpr uint32_t GF_P1_MAX = 3037000499u;  // floor(sqrt(2^63 - 25))
+
+template <bool B>
+struct BoolC { static constexpr bool value = B; };
+
+// f(BoolC<GF>) with GF = "this instance may use the fused Garner".  Branches
+// once per thread, outside the draw loop, so each loop body is straight-line.
+template <class F>
+RSA_DEV void with_garner(const FastInst& P, F&& f) {
+#if RSA_GARNER_FUSED
+    if (P.p1 <= GF_P1_MAX) { f(BoolC<true>{}); return; }
+#endif
+    f(BoolC<false>{});
+}
 
 RSA_DEV FastInst load_fast(const rsa_instance* __restrict__ ip) {
     FastInst P;
@@ -26,6 +50,8 @@ RSA_DEV FastInst load_fast(const rsa_instance* __restrict__ ip) {
     P.p1 = w0.x; P.p2 = w0.y; P.p1_inv = w0.z; P.p2_inv = w0.w;
     P.a = w1.x; P.e = w1.y; P.k1 = w1.z; P.k2 = w1.w;
     P.r2_1 = w2.x; P.r2_2 = w2.y; P.garner = w2.z;
+    P.gA = mont_mul(P.k1, P.garner, P.p1, P.p1_inv);  // k1 * p2inv mod p1
+    P.gB = P.p1 - P.garner;                            // -p2inv * R mod p1 (garner != 0)
     P.p2d = (double)P.p2;
     P.n_float = __ldg(&ip->n_float);
     P.n_recip = __ldg(&ip->n_recip);
@@ -60,24 +86,39 @@ RSA_DEV uint32_t pow_e(uint32_t x, uint32_t e, uint32_t p, uint32_t pinv) {
 
 // One draw on the fast path: advances the lane and returns (h, c2) with the
 // ciphertext c = h*p2 + c2, h = (c1 - c2)*p2inv mod p1 (Garner).
-template <uint32_t E>
+// GF: h = REDC(y1*A + c2r*B) with A = k1 p2inv, B = -p2inv R (mod p1), since
+// y1 k1 R^-1 = c1: one REDC of a two-product sum (7 heavy slots) replaces the
+// k1 product + Garner product (10 slots) and the sub_mod between them.  The
+// sum is < 2 p1^2 < 2^64 and its REDC lies in (-p1, 2^32) < 2 p1, so one
+// conditional add or subtract makes h canonical.
+template <uint32_t E, bool GF = false>
 RSA_DEV void draw_fast_hc(const FastInst& P, Lane& L, uint32_t& h, uint32_t& c2) {
     L.s = skip_q63(L.s, P.a);
     L.x1 = add_mod(L.x1, mont_redc(L.s, P.p1, P.p1_inv), P.p1);
     L.x2 = add_mod(L.x2, mont_redc(L.s, P.p2, P.p2_inv), P.p2);
     uint32_t y1 = pow_e<E>(L.x1, P.e, P.p1, P.p1_inv);   // m1^e R^-(2e-1)
     uint32_t y2 = pow_e<E>(L.x2, P.e, P.p2, P.p2_inv);
-    uint32_t c1 = mont_mul(y1, P.k1, P.p1, P.p1_inv);    // m1^e mod p1
     c2 = mont_mul(y2, P.k2, P.p2, P.p2_inv);             // m2^e mod p2
     uint32_t c2r = c2 >= P.p1 ? c2 - P.p1 : c2;          // c2 < 2^32 < 2 p1
-    uint32_t d = sub_mod(c1, c2r, P.p1);
-    h = mont_mul(d, P.garner, P.p1, P.p1_inv);           // d * p2inv mod p1
+    if constexpr (GF) {
+        uint64_t t = (uint64_t)y1 * P.gA + (uint64_t)c2r * P.gB;  // < 2 p1^2 < 2^64
+        uint32_t m = (uint32_t)t * P.p1_inv;
+        uint32_t u = __umulhi(m, P.p1);
+        uint32_t th = (uint32_t)(t >> 32);
+        uint32_t r = th - u;
+        r = th < u ? r + P.p1 : r;
+        h = r >= P.p1 ? r - P.p1 : r;
+    } else {
+        uint32_t c1 = mont_mul(y1, P.k1, P.p1, P.p1_inv);  // m1^e mod p1
+        uint32_t d = sub_mod(c1, c2r, P.p1);
+        h = mont_mul(d, P.garner, P.p1, P.p1_inv);         // d * p2inv mod p1
+    }
 }
 
-template <uint32_t E>
+template <uint32_t E, bool GF = false>
 RSA_DEV uint64_t draw_fast(const FastInst& P, Lane& L) {
     uint32_t h, c2;
-    draw_fast_hc<E>(P, L, h, c2);
+    draw_fast_hc<E, GF>(P, L, h, c2);
     return (uint64_t)h * P.p2 + c2;
 }
 

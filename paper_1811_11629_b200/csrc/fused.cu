@@ -54,37 +54,44 @@ k_fused(const rsa_instance* __restrict__ inst, uint32_t n_inst, uint64_t draws,
     double s1 = 0.0, s2 = 0.0, lag = 0.0, xy = 0.0, prev = 0.0, first = 0.0;
     // chunks of <= 2^15 draws: the u16 counters cannot wrap inside a chunk, and
     // the inner loop carries no flush test
-    for (uint64_t done = 0; done < draws;) {
-        const uint64_t left = draws - done;
-        const uint32_t len = (uint32_t)(left < FLUSH_MASK + 1 ? left : FLUSH_MASK + 1);
-        uint32_t kk = 0;
-        if (done == 0) {  // peeled first draw: r_0 is reported, no lag term yet
-            double r = to_unit(draw_fast<E>(P, L), P.n_float, P.n_recip, P.n_recip_lo);
-            first = r;
-            s1 = r;
-            s2 = __dmul_rn(r, r);
-            double o = __shfl_xor_sync(0xffffffffu, r, 1);
-            xy = __dmul_rn(r, o);
-            hb[(uint32_t)__double2loint(__fma_rz(r, 64.0, 0x1p52)) * FUSED_BLOCK] += 1;
-            prev = r;
-            kk = 1;
+    // the partner-stream shuffles need the whole warp on one loop body
+    const bool gf = RSA_GARNER_FUSED && __all_sync(0xffffffffu, P.p1 <= GF_P1_MAX);
+    auto run = [&](auto gfc) {
+        constexpr bool GF = decltype(gfc)::value;
+        for (uint64_t done = 0; done < draws;) {
+            const uint64_t left = draws - done;
+            const uint32_t len = (uint32_t)(left < FLUSH_MASK + 1 ? left : FLUSH_MASK + 1);
+            uint32_t kk = 0;
+            if (done == 0) {  // peeled first draw: r_0 is reported, no lag term yet
+                double r = to_unit(draw_fast<E, GF>(P, L), P.n_float, P.n_recip, P.n_recip_lo);
+                first = r;
+                s1 = r;
+                s2 = __dmul_rn(r, r);
+                double o = __shfl_xor_sync(0xffffffffu, r, 1);
+                xy = __dmul_rn(r, o);
+                hb[(uint32_t)__double2loint(__fma_rz(r, 64.0, 0x1p52)) * FUSED_BLOCK] += 1;
+                prev = r;
+                kk = 1;
+            }
+    #pragma unroll 2
+            for (; kk < len; ++kk) {
+                double r = to_unit(draw_fast<E, GF>(P, L), P.n_float, P.n_recip, P.n_recip_lo);
+                s1 += r;
+                s2 = __fma_rn(r, r, s2);
+                lag = __fma_rn(prev, r, lag);
+                prev = r;
+                double o = __shfl_xor_sync(0xffffffffu, r, 1);
+                xy = __fma_rn(r, o, xy);
+                // floor(64 r) exactly: 2^52 + 64r rounded toward zero keeps the integer part
+                uint32_t b = (uint32_t)__double2loint(__fma_rz(r, 64.0, 0x1p52));
+                hb[b * FUSED_BLOCK] += 1;
+            }
+            done += len;
+            flush_hist(h, gh, active);
         }
-#pragma unroll 2
-        for (; kk < len; ++kk) {
-            double r = to_unit(draw_fast<E>(P, L), P.n_float, P.n_recip, P.n_recip_lo);
-            s1 += r;
-            s2 = __fma_rn(r, r, s2);
-            lag = __fma_rn(prev, r, lag);
-            prev = r;
-            double o = __shfl_xor_sync(0xffffffffu, r, 1);
-            xy = __fma_rn(r, o, xy);
-            // floor(64 r) exactly: 2^52 + 64r rounded toward zero keeps the integer part
-            uint32_t b = (uint32_t)__double2loint(__fma_rz(r, 64.0, 0x1p52));
-            hb[b * FUSED_BLOCK] += 1;
-        }
-        done += len;
-        flush_hist(h, gh, active);
-    }
+    };
+    if (gf) run(BoolC<true>{});
+    else run(BoolC<false>{});
     if (active) {
         rsa_fused_stat st;
         st.s1 = s1; st.s2 = s2; st.lag = lag; st.first = first; st.last = prev; st.xy = xy;

@@ -168,11 +168,14 @@ k_seg_fill(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t lanes, u
     Ln.x1 = add_mod(Ln.x1, prefix[2 * t], P.p1);
     Ln.x2 = add_mod(Ln.x2, prefix[2 * t + 1], P.p2);
     uint64_t off = i * inst_stride + k0 * mv + g;
-    for (uint64_t k = 0; k < len; ++k, off += mv) {
-        const uint64_t c = draw_fast<E>(P, Ln);
-        if constexpr (RAW) __stcs(reinterpret_cast<unsigned long long*>(raw + off), (unsigned long long)c);
-        if constexpr (F64) __stcs(f64 + off, to_unit(c, P.n_float, P.n_recip, P.n_recip_lo));
-    }
+    with_garner(P, [&](auto gf) {
+        constexpr bool GF = decltype(gf)::value;
+        for (uint64_t k = 0; k < len; ++k, off += mv) {
+            const uint64_t c = draw_fast<E, GF>(P, Ln);
+            if constexpr (RAW) __stcs(reinterpret_cast<unsigned long long*>(raw + off), (unsigned long long)c);
+            if constexpr (F64) __stcs(f64 + off, to_unit(c, P.n_float, P.n_recip, P.n_recip_lo));
+        }
+    });
     if (j == nseg - 1) {  // the last segment owns the lane's final state
         m1[lane] = lane_m1(P, Ln);
         m2[lane] = lane_m2(P, Ln);

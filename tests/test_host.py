@@ -165,3 +165,44 @@ def test_shard_range():
             assert s0 + c0 == s1
         assert sum(c for _, c in spans) == total
         assert all(s % align == 0 and c % align == 0 for s, c in spans)
+
+
+def test_fused_garner_bound():
+    """csrc/draw.cuh draw_fast_hc<E, true>: h = REDC(y1*A + c2r*B) mod p1 with
+    A = k1*p2inv, B = -p2inv*R (mod p1) equals the two-product Garner
+    (c1 - c2)*p2inv mod p1 (rsacore.py:207-210), the 64-bit sum never
+    overflows and one conditional add/subtract makes h canonical, for p1 up to
+    floor(sqrt q) (the largest p1 paramfactory.py:27-30 can produce) — checked
+    with Python ints at the extremes of every operand."""
+    import random
+    R32, M32 = 1 << 32, (1 << 32) - 1
+    q = (1 << 63) - 25
+    gf_max = 3037000499
+    assert gf_max * gf_max <= q < (gf_max + 1) ** 2
+    rng = random.Random(7)
+    for p1 in (gf_max, gf_max - 2, (1 << 31) + 11, 2663418827):
+        p1inv = pow(p1, -1, R32)
+        for _ in range(300):
+            p2 = rng.randrange(1 << 31, 1 << 32) | 1
+            try:
+                p2inv = pow(p2, -1, p1)
+            except ValueError:
+                continue
+            e = 9
+            k1 = pow(R32, 2 * e, p1)
+            garner = p2inv * R32 % p1
+            A = k1 * garner * pow(R32, -1, p1) % p1
+            B = p1 - garner
+            for y1, c2 in ((p1 - 1, p2 - 1), (p1 - 1, p1 - 1), (0, 0),
+                           (rng.randrange(p1), rng.randrange(p2))):
+                c2r = c2 - p1 if c2 >= p1 else c2
+                t = y1 * A + c2r * B
+                assert t < 1 << 64
+                m = (t & M32) * p1inv & M32
+                u = m * p1 >> 32
+                th = t >> 32
+                r = (th - u) & M32
+                r = (r + p1) & M32 if th < u else r
+                h = r - p1 if r >= p1 else r
+                c1 = y1 * k1 * pow(R32, -1, p1) % p1
+                assert h == (c1 - c2) * p2inv % p1

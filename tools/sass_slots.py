@@ -10,7 +10,7 @@ import sys
 from collections import Counter
 
 lines = open(sys.argv[1]).read().splitlines()
-if len(sys.argv) > 3:
+if len([x for x in sys.argv if not x.startswith('--')]) > 3:
     lines = lines[int(sys.argv[2]) - 1:int(sys.argv[3])]
 else:
     # the hot loop: among innermost loops (no backward branch inside), the one
@@ -24,15 +24,27 @@ else:
             loops.append((i0, i))
     inner = [(a, b) for a, b in loops if not any(a <= c and d < b and (c, d) != (a, b) for c, d in loops)]
 
-    def weight(span):
+    def weight(span):  # heavy-datapath slots, the weights below
         w = 0
         for l in lines[span[0]:span[1] + 1]:
             mm = re.search(r"\*/\s+(?:@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]*)", l)
-            if mm and mm.group(1).startswith(("IMAD", "DFMA", "DMUL")):
+            if not mm:
+                continue
+            op = mm.group(1)
+            if op.startswith(("IMAD.WIDE", "IMAD.HI")):
+                w += 2
+            elif op.startswith(("IMAD", "DFMA", "DMUL", "DADD", "DSETP", "DMNMX")):
                 w += 1
         return w
 
-    a, b = max(inner, key=weight)
+    # kernels with a per-instance fast/fallback split (the fused Garner,
+    # draw.cuh with_garner) carry two draw loops: the fast one is the lighter
+    # of the loops within 60 % of the heaviest ("--lightest"; default heaviest)
+    top = max(weight(x) for x in inner)
+    if "--lightest" in sys.argv:
+        a, b = min((x for x in inner if weight(x) >= 0.6 * top), key=weight)
+    else:
+        a, b = max(inner, key=weight)
     lines = lines[a:b + 1]
 ops = Counter()
 heavy = 0.0

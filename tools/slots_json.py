@@ -19,7 +19,7 @@ def count(fn: str) -> float:
     path = "/tmp/_slots.txt"
     with open(path, "w") as fh:
         fh.write("\n".join(lines))
-    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sass_slots.py"), path],
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sass_slots.py"), path, "--lightest"],
                          capture_output=True, text=True).stdout.splitlines()[0]
     return float(re.search(r"heavy slots ([0-9.]+)", out).group(1))
 
