@@ -78,6 +78,23 @@ RSA_DEV Lane lane_in(const FastInst& P, uint64_t m1, uint64_t m2, uint64_t s) {
 RSA_DEV uint64_t lane_m1(const FastInst& P, const Lane& L) { return mont_mul(L.x1, P.r2_1, P.p1, P.p1_inv); }
 RSA_DEV uint64_t lane_m2(const FastInst& P, const Lane& L) { return mont_mul(L.x2, P.r2_2, P.p2, P.p2_inv); }
 
+// A/B knobs (tools/ab, profiles/r01_ab_msg_fl.txt): both variants cut heavy
+// slots but measured slower, so the defaults stay 0.
+#ifndef RSA_MSG_VARIANT
+#define RSA_MSG_VARIANT 0
+#endif
+// x + REDC(s) mod p (the message step in the R^-1 domain, vecgen.py:94-95).
+RSA_DEV uint32_t msg_add(uint32_t x, uint64_t s, uint32_t p, uint32_t pinv) {
+#if RSA_MSG_VARIANT == 0
+    return add_mod(x, mont_redc(s, p, pinv), p);
+#else  // carry-flag add: -5 heavy slots per 2 draws at e=3, measured 2 % slower
+    uint32_t y = mont_redc(s, p, pinv);
+    uint32_t r, c;
+    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, 0, 0;" : "=r"(r), "=r"(c) : "r"(x), "r"(y));
+    return (c | (uint32_t)(r >= p)) ? r - p : r;
+#endif
+}
+
 template <uint32_t E>
 RSA_DEV uint32_t pow_e(uint32_t x, uint32_t e, uint32_t p, uint32_t pinv) {
     if constexpr (E != 0) return Chain<E>::pow(x, p, pinv);
@@ -94,8 +111,8 @@ RSA_DEV uint32_t pow_e(uint32_t x, uint32_t e, uint32_t p, uint32_t pinv) {
 template <uint32_t E, bool GF = false>
 RSA_DEV void draw_fast_hc(const FastInst& P, Lane& L, uint32_t& h, uint32_t& c2) {
     L.s = skip_q63(L.s, P.a);
-    L.x1 = add_mod(L.x1, mont_redc(L.s, P.p1, P.p1_inv), P.p1);
-    L.x2 = add_mod(L.x2, mont_redc(L.s, P.p2, P.p2_inv), P.p2);
+    L.x1 = msg_add(L.x1, L.s, P.p1, P.p1_inv);
+    L.x2 = msg_add(L.x2, L.s, P.p2, P.p2_inv);
     uint32_t y1 = pow_e<E>(L.x1, P.e, P.p1, P.p1_inv);   // m1^e R^-(2e-1)
     uint32_t y2 = pow_e<E>(L.x2, P.e, P.p2, P.p2_inv);
     c2 = mont_mul(y2, P.k2, P.p2, P.p2_inv);             // m2^e mod p2
@@ -120,6 +137,23 @@ RSA_DEV uint64_t draw_fast(const FastInst& P, Lane& L) {
     uint32_t h, c2;
     draw_fast_hc<E, GF>(P, L, h, c2);
     return (uint64_t)h * P.p2 + c2;
+}
+
+#ifndef RSA_FL_FMA
+#define RSA_FL_FMA 0
+#endif
+// One draw mapped to r = min(fl(c)/fl(n), 1-2^-53) (vecgen.py:103-107) when
+// the ciphertext itself is not needed: fl(c) = RN(h*p2 + c2) is one FMA of
+// exactly representable operands (RSA_FL_FMA), else I2F of the 64-bit c.
+template <uint32_t E, bool GF>
+RSA_DEV double draw_unit(const FastInst& P, Lane& L) {
+#if RSA_FL_FMA
+    uint32_t h, c2;
+    draw_fast_hc<E, GF>(P, L, h, c2);
+    return unit_from_fl(__fma_rn((double)h, P.p2d, (double)c2), P.n_float, P.n_recip, P.n_recip_lo);
+#else
+    return to_unit(draw_fast<E, GF>(P, L), P.n_float, P.n_recip, P.n_recip_lo);
+#endif
 }
 
 // ---- general path (test-mode sizes, any prime q, unit/const skip) -------------

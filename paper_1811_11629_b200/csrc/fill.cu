@@ -68,17 +68,24 @@ k_fill_fast(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t total_l
     with_garner(P, [&](auto gf) {
         constexpr bool GF = decltype(gf)::value;
         for (uint64_t k = 0; k < blocks; ++k, off += step) {
-            uint64_t c[LPT];
+            if constexpr (!RAW && F64 == 1 && RSA_FL_FMA) {
+                double r[LPT];  // float-only fill: fl(c) by one FMA (draw_unit)
 #pragma unroll
-            for (int j = 0; j < LPT; ++j) c[j] = draw_fast<E, GF>(P, L[j]);
-            if constexpr (RAW) store_u64<LPT>(raw + off, c);
-            if constexpr (F64 != 0) {
-                double r[LPT];
-#pragma unroll
-                for (int j = 0; j < LPT; ++j)
-                    r[j] = F64 == 1 ? to_unit(c[j], P.n_float, P.n_recip, P.n_recip_lo)
-                                    : __uint2double_rn((uint32_t)c[j]) * 0x1p-32;
+                for (int j = 0; j < LPT; ++j) r[j] = draw_unit<E, GF>(P, L[j]);
                 store_f64<LPT>(f64 + off, r);
+            } else {
+                uint64_t c[LPT];
+#pragma unroll
+                for (int j = 0; j < LPT; ++j) c[j] = draw_fast<E, GF>(P, L[j]);
+                if constexpr (RAW) store_u64<LPT>(raw + off, c);
+                if constexpr (F64 != 0) {
+                    double r[LPT];
+#pragma unroll
+                    for (int j = 0; j < LPT; ++j)
+                        r[j] = F64 == 1 ? to_unit(c[j], P.n_float, P.n_recip, P.n_recip_lo)
+                                        : __uint2double_rn((uint32_t)c[j]) * 0x1p-32;
+                    store_f64<LPT>(f64 + off, r);
+                }
             }
         }
     });

@@ -63,7 +63,7 @@ k_fused(const rsa_instance* __restrict__ inst, uint32_t n_inst, uint64_t draws,
             const uint32_t len = (uint32_t)(left < FLUSH_MASK + 1 ? left : FLUSH_MASK + 1);
             uint32_t kk = 0;
             if (done == 0) {  // peeled first draw: r_0 is reported, no lag term yet
-                double r = to_unit(draw_fast<E, GF>(P, L), P.n_float, P.n_recip, P.n_recip_lo);
+                double r = draw_unit<E, GF>(P, L);
                 first = r;
                 s1 = r;
                 s2 = __dmul_rn(r, r);
@@ -75,7 +75,7 @@ k_fused(const rsa_instance* __restrict__ inst, uint32_t n_inst, uint64_t draws,
             }
     #pragma unroll 2
             for (; kk < len; ++kk) {
-                double r = to_unit(draw_fast<E, GF>(P, L), P.n_float, P.n_recip, P.n_recip_lo);
+                double r = draw_unit<E, GF>(P, L);
                 s1 += r;
                 s2 = __fma_rn(r, r, s2);
                 lag = __fma_rn(prev, r, lag);
