@@ -201,6 +201,7 @@ def device_instance(params: GeneratorParams, dev=None) -> torch.Tensor:
     return _device_instance_cached(params, d.index)
 
 
+@functools.lru_cache(maxsize=256)
 def instance_flags(params: GeneratorParams) -> int:
     return int(_instance_record(params)[0]["flags"])
 
@@ -232,18 +233,24 @@ def init(params: GeneratorParams, m0: int = 0, s0: int = 1) -> GeneratorState:
 
 
 def _scalar_run(state: GeneratorState, params: GeneratorParams, count: int, raw: bool, f64: bool,
-                dev=None):
+                dev=None) -> np.ndarray:
+    """count draws of the one-lane stream on the GPU; returns the host array
+    (uint64 ciphertexts, or float64) and advances `state`.  One H2D of the
+    3-word state and one D2H of state + outputs: a single round trip."""
     d = _device.device(dev)
     inst = device_instance(params, d)
     s_in = 1 if params.skip_mode == SKIP_UNIT else state.s
-    st = _device.u64([state.m1, state.m2, s_in], d)
-    m1, m2, s = st[0:1], st[1:2], st[2:3]
-    out_raw = torch.empty(count, dtype=torch.uint64, device=d) if raw else None
-    out_f64 = torch.empty(count, dtype=torch.float64, device=d) if f64 else None
+    n_out = count if (raw or f64) else 0
+    # uint64 words carried bit-for-bit in an int64 tensor (a const skip may exceed 2^63)
+    buf = torch.empty(3 + n_out, dtype=torch.int64, device=d)
+    buf[:3].copy_(torch.from_numpy(np.array([state.m1, state.m2, s_in], dtype=np.uint64).view(np.int64)))
+    ptr = buf.data_ptr()
+    m1, m2, s = ptr, ptr + 8, ptr + 16
+    out = ptr + 24 if n_out else None
     if count:
         flags = instance_flags(params)
-        args = (inst.data_ptr(), 1, 1, count, params.e, flags, m1.data_ptr(), m2.data_ptr(), s.data_ptr(),
-                out_raw.data_ptr() if raw else None, out_f64.data_ptr() if f64 else None, count)
+        args = (inst.data_ptr(), 1, 1, count, params.e, flags, m1, m2, s,
+                out if raw else None, out if f64 else None, count)
         L = _lib.load()
         if flags & _lib.RSA_FLAG_FAST and (raw or f64) and int(L.rsa_fill_segments(1, count)) > 1:
             # one lane, many draws: split it across threads (K1s, bit-identical)
@@ -252,12 +259,14 @@ def _scalar_run(state: GeneratorState, params: GeneratorParams, count: int, raw:
             _lib.call("rsa_fill_segmented", *args, scratch.data_ptr(), nb, _device.stream(d))
         else:
             _lib.call("rsa_fill", *args, _device.stream(d))
-    new = _device.to_ints(st)
+    host = buf.cpu().numpy().view(np.uint64)
+    new = host[:3].tolist()
     state.m1, state.m2 = new[0], new[1]
     if params.skip_mode == SKIP_LCG or (params.skip_mode == SKIP_UNIT and count):
         state.s = new[2]
     state.draws += count
-    return out_raw, out_f64
+    body = host[3:]
+    return body.view(np.float64) if f64 else body
 
 
 def next_raw(state: GeneratorState, params: GeneratorParams) -> int:
@@ -272,14 +281,12 @@ def next_f64(state: GeneratorState, params: GeneratorParams) -> float:
 
 def take_raws(state: GeneratorState, params: GeneratorParams, count: int) -> list[int]:
     """count sequential raw draws (rsacore.py:236-258)."""
-    raw, _ = _scalar_run(state, params, count, True, False)
-    return _device.to_ints(raw)
+    return _scalar_run(state, params, count, True, False).tolist()
 
 
 def take_floats(state: GeneratorState, params: GeneratorParams, count: int) -> list[float]:
     """count sequential next_f64 draws (rsacore.py:261-264)."""
-    _, f = _scalar_run(state, params, count, False, True)
-    return f.cpu().numpy().tolist()
+    return _scalar_run(state, params, count, False, True).tolist()
 
 
 def decrypt(c: int, params: GeneratorParams) -> int:

@@ -20,3 +20,23 @@ t = time.perf_counter()
 for i in range(200):
     R.rsacore.take_raws(st, p, 16)
 print("take_raws(16) ms", (time.perf_counter() - t) / 200 * 1e3)
+t = time.perf_counter()
+for i in range(200):
+    R.rsacore.next_raw(st, p)
+print("next_raw ms", (time.perf_counter() - t) / 200 * 1e3)
+t = time.perf_counter()
+for i in range(50):
+    R.rsacore.take_floats(st, p, 1 << 16)
+print("rsacore.take_floats(2^16) ms", (time.perf_counter() - t) / 50 * 1e3)
+for mv in (1, 64, 65536):
+    v = R.init_vector(p, mv=mv)
+    out = torch.empty(1 << 20, dtype=torch.float64, device="cuda")
+    R.take_floats(v, 1 << 20, out=out)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for i in range(50):
+        R.take_floats(v, 1 << 20, out=out)
+    t_host = (time.perf_counter() - t) / 50 * 1e3
+    torch.cuda.synchronize()
+    t_all = (time.perf_counter() - t) / 50 * 1e3
+    print(f"vecgen.take_floats(2^20, mv={mv}) host-call ms {t_host:.4f}  incl. sync ms {t_all:.4f}")
