@@ -196,4 +196,38 @@ def run_other(args, world, rank, local):
     line["phases"] = {"scan_ms": scan_ms, "scan_gcandidates_s": cands / world / (scan_ms * 1e-3) / 1e9,
                       "safe_primes_found": phase["count"], "setup_ms": setup_ms,
                       "tuples_per_s": n / (setup_ms * 1e-3)}
+    if world == 1:
+        line["literal_mr"] = literal_mr_scan(args, lo, hi, dev, phase["count"])
     return line
+
+
+def literal_mr_scan(args, lo, hi, dev, want_count):
+    """The census exactly as BASELINE config 5 words it (MR 2, 7, 61 on every
+    odd n and on (n-1)/2; rsa_safe_prime_scan_mr), timed beside the production
+    scan.  Roofline: SURVEY §8(d)'s 55.5 Montgomery products per odd candidate
+    against the in-run Montgomery-triple probe (products/s)."""
+    import torch
+    from bench import probe_imad_peak
+    from paper_1811_11629_b200 import paramfactory
+    st = torch.cuda.current_stream()
+    paramfactory.safe_primes_u32(lo, hi, dev, literal_mr=True)  # warm-up
+    times = []
+    for _ in range(max(1, min(args.steps, 3))):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        sp = paramfactory.safe_primes_u32(lo, hi, dev, literal_mr=True)
+        b.record(st)
+        b.synchronize()
+        times.append(a.elapsed_time(b))
+    ms = statistics.median(times)
+    cands = (hi - lo) // 2
+    products = 55.5 * cands
+    peak = probe_imad_peak(dev)["ops_per_s"] / 3.0  # Montgomery triples (products) per second
+    return {"ms": ms, "gcandidates_s": cands / (ms * 1e-3) / 1e9, "safe_primes_found": int(sp.numel()),
+            "equal_count": int(sp.numel()) == want_count,
+            "roofline": {"bound": "imad", "kernel": "k_mr_base2 + k_mr_rest",
+                         "achieved": products / (ms * 1e-3) / 1e12, "peak": peak / 1e12,
+                         "unit": "T Montgomery products/s", "frac": products / (ms * 1e-3) / peak,
+                         "algorithmic_products_per_candidate": 55.5},
+            "note": "literal MR(2,7,61) census (no sieve, no pseudoprime table); the production scan "
+                    "(phases.scan_ms) returns the same list"}

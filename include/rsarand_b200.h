@@ -182,6 +182,18 @@ int rsa_safe_prime_scan(uint64_t lo, uint64_t hi, uint32_t* out, uint64_t out_ca
                         uint64_t* count, void* scratch, uint64_t scratch_bytes,
                         void* stream);
 
+/* The same census by the reference algorithm as BASELINE config 5 states it:
+ * deterministic Miller-Rabin with bases 2, 7, 61 (exact below 4,759,123,141)
+ * on every odd n in [lo, hi) and on (n-1)/2 (numtheory.py:60-98,
+ * paramfactory.py:105-130; n < 10201 by trial division).  No sieve, no
+ * pseudoprime table: a cross-check of rsa_safe_prime_scan and the IMAD-bound
+ * yardstick it is measured against.  Same output contract as
+ * rsa_safe_prime_scan; scratch >= rsa_safe_prime_scan_mr_scratch_bytes. */
+uint64_t rsa_safe_prime_scan_mr_scratch_bytes(uint64_t lo, uint64_t hi);
+int rsa_safe_prime_scan_mr(uint64_t lo, uint64_t hi, uint32_t* out, uint64_t out_cap,
+                           uint64_t* count, void* scratch, uint64_t scratch_bytes,
+                           void* stream);
+
 /* Batched is_prime / is_safe_prime predicates (numtheory.py:81-98) for 32-bit n. */
 int rsa_is_safe_prime32(const uint32_t* n, uint64_t count, uint8_t* is_prime,
                         uint8_t* is_safe, void* stream);

@@ -73,6 +73,8 @@ PROTOTYPES = {
     "rsa_fused_pool": (ctypes.c_int, [c_vp, c_vp, c_u32, c_vp, c_vp, c_vp]),
     "rsa_safe_prime_scan_scratch_bytes": (c_u64, [c_u64, c_u64]),
     "rsa_safe_prime_scan": (ctypes.c_int, [c_u64, c_u64, c_vp, c_u64, c_vp, c_vp, c_u64, c_vp]),
+    "rsa_safe_prime_scan_mr_scratch_bytes": (c_u64, [c_u64, c_u64]),
+    "rsa_safe_prime_scan_mr": (ctypes.c_int, [c_u64, c_u64, c_vp, c_u64, c_vp, c_vp, c_u64, c_vp]),
     "rsa_is_safe_prime32": (ctypes.c_int, [c_vp, c_u64, c_vp, c_vp, c_vp]),
     "rsa_safe_prime_index": (ctypes.c_int, [c_vp, c_u64, c_vp, c_vp]),
     "rsa_find_pair": (ctypes.c_int, [c_vp, c_u64, c_u64, c_u64, c_vp, c_u64, c_vp, c_vp, c_vp, c_vp]),

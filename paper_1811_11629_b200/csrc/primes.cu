@@ -635,6 +635,163 @@ k_scan_write(ScanRange R, const uint32_t* __restrict__ words, uint64_t ranges,
     }
 }
 
+// ---- literal scan: deterministic Miller-Rabin (2, 7, 61) on every odd n ----
+//
+// The BASELINE config-5 statement of the census: every odd n in [lo, hi) is
+// tested with MR bases 2, 7, 61 (exact below 4,759,123,141) and so is
+// (n-1)/2 when it is odd (numtheory.py:60-98 semantics; an even (n-1)/2 is
+// rejected before MR).  No sieve and no pseudoprime table: this is the
+// reference algorithm restated for the GPU, kept beside the production scan
+// (rsa_safe_prime_scan) as its cross-check and as the IMAD-bound yardstick
+// the sieve is measured against.  Two compacted stages per chunk so warps do
+// not idle on their few prime lanes: (1) base 2 on every odd n, passers
+// listed; (2) bases 7 and 61 on n, then 2, 7, 61 on (n-1)/2; verdicts go into
+// the same candidate bitmask, whose count / offsets / ordered write are the
+// production tail.
+
+// g*R mod n for a small base g (binary method with modular doublings)
+RSA_DEV uint32_t small_times_r(uint32_t g, uint32_t onem, uint32_t n) {
+    uint32_t x = onem;
+    for (int b = 30 - __clz(g); b >= 0; --b) {
+        x = add_mod(x, x, n);
+        if ((g >> b) & 1u) x = add_mod(x, onem, n);
+    }
+    return x;
+}
+
+// strong probable-prime test to the small base g of K odd n > g, interleaved
+template <int K>
+RSA_DEV void sprp_multi(const uint32_t (&n)[K], uint32_t g, bool (&ok)[K]) {
+    uint32_t ninv[K], onem[K], gm[K], d[K], x[K];
+    int u[K];
+    uint32_t dall = 0;
+    int umax = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        ninv[k] = inv32(n[k]);
+        onem[k] = r_mod(n[k]);
+        gm[k] = small_times_r(g, onem[k], n[k]);
+        d[k] = n[k] - 1;
+        u[k] = __ffs(d[k]) - 1;
+        d[k] >>= u[k];
+        x[k] = onem[k];
+        dall |= d[k];
+        umax = max(umax, u[k]);
+    }
+    for (int b = 31 - __clz(dall); b >= 0; --b) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            x[k] = mont_mul(x[k], x[k], n[k], ninv[k]);
+            if ((d[k] >> b) & 1u) x[k] = mont_mul(x[k], gm[k], n[k], ninv[k]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) ok[k] = x[k] == onem[k] || x[k] == n[k] - onem[k];
+    for (int j = 1; j < umax; ++j) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            x[k] = mont_mul(x[k], x[k], n[k], ninv[k]);
+            ok[k] = ok[k] || (j < u[k] && x[k] == n[k] - onem[k]);
+        }
+    }
+}
+
+// bitmask index of n in the scan's candidate sequence ({5, 7} u first + 12 j), or ~0
+RSA_DEV uint64_t cand_index(const ScanRange& R, uint32_t n) {
+    for (uint32_t k = 0; k < R.nspec; ++k)
+        if (R.spec[k] == n) return k;
+    if (n < R.first || (n - R.first) % 12 != 0) return ~0ull;
+    return R.nspec + (n - R.first) / 12;
+}
+
+constexpr uint32_t MR_SMALL = 10201u;  // below: trial division decides (no base reaches n)
+
+// stage 1: odd n = lo_odd + 2 i, i in [i0, i1): base-2 SPRP, passers listed
+__global__ void __launch_bounds__(SCAN_BLOCK)
+k_mr_base2(ScanRange R, uint64_t lo_odd, uint64_t i0, uint64_t i1, uint32_t* __restrict__ list,
+           uint32_t* __restrict__ nlist, uint32_t* __restrict__ words) {
+    const uint64_t tile = (uint64_t)SPRP_ILP * SCAN_BLOCK, stride = (uint64_t)gridDim.x * tile;
+    const int lane = threadIdx.x & 31;
+    for (uint64_t b0 = i0 + blockIdx.x * tile; b0 < i1; b0 += stride) {
+        uint32_t v[SPRP_ILP];
+        bool ok[SPRP_ILP], in[SPRP_ILP];
+#pragma unroll
+        for (int k = 0; k < SPRP_ILP; ++k) {
+            const uint64_t i = b0 + k * SCAN_BLOCK + threadIdx.x;
+            const uint64_t n = lo_odd + 2 * i;
+            in[k] = i < i1;
+            v[k] = in[k] && n >= MR_SMALL ? (uint32_t)n : SPRP_DUMMY;
+            if (in[k] && n < MR_SMALL) {  // small n: exact by trial division
+                in[k] = false;
+                if (is_safe_prime32((uint32_t)n)) {
+                    const uint64_t j = cand_index(R, (uint32_t)n);
+                    if (j != ~0ull) atomicOr(&words[j >> 5], 1u << (j & 31));
+                }
+            }
+        }
+        sprp2_multi<SPRP_ILP>(v, ok);
+        uint32_t bal[SPRP_ILP], tot = 0;
+#pragma unroll
+        for (int k = 0; k < SPRP_ILP; ++k) {
+            ok[k] = ok[k] && in[k];
+            bal[k] = __ballot_sync(0xffffffffu, ok[k]);
+            tot += __popc(bal[k]);
+        }
+        uint32_t pos = 0;
+        if (lane == 0 && tot) pos = atomicAdd(nlist, tot);
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        const uint32_t below = (1u << lane) - 1;
+#pragma unroll
+        for (int k = 0; k < SPRP_ILP; ++k) {
+            if (ok[k]) list[pos + __popc(bal[k] & below)] = v[k];
+            pos += __popc(bal[k]);
+        }
+    }
+}
+
+// stage 2: bases 7, 61 on n; then 2, 7, 61 on q = (n-1)/2 (odd q only)
+__global__ void __launch_bounds__(SCAN_BLOCK)
+k_mr_rest(ScanRange R, const uint32_t* __restrict__ list, const uint32_t* __restrict__ nlist,
+          uint32_t* __restrict__ words) {
+    const uint32_t n = *nlist;
+    const uint32_t tile = SPRP_ILP * SCAN_BLOCK, stride = gridDim.x * tile;
+    for (uint32_t b0 = blockIdx.x * tile; b0 < n; b0 += stride) {
+        uint32_t v[SPRP_ILP], q[SPRP_ILP];
+        bool ok[SPRP_ILP], t[SPRP_ILP];
+#pragma unroll
+        for (int k = 0; k < SPRP_ILP; ++k) {
+            const uint32_t i = b0 + k * SCAN_BLOCK + threadIdx.x;
+            v[k] = i < n ? list[i] : SPRP_DUMMY;
+        }
+        sprp_multi<SPRP_ILP>(v, 7, ok);
+        sprp_multi<SPRP_ILP>(v, 61, t);
+#pragma unroll
+        for (int k = 0; k < SPRP_ILP; ++k) {
+            // p prime; (p-1)/2 even (p = 1 mod 4) is rejected before MR
+            ok[k] = ok[k] && t[k] && (v[k] & 3u) == 3u && b0 + k * SCAN_BLOCK + threadIdx.x < n;
+            q[k] = ok[k] ? v[k] >> 1 : SPRP_DUMMY;
+        }
+        // the warp runs the q tests only when one of its lanes needs them
+        if (__any_sync(0xffffffffu, ok[0] || (SPRP_ILP > 1 && ok[SPRP_ILP - 1]))) {
+            sprp2_multi<SPRP_ILP>(q, t);
+#pragma unroll
+            for (int k = 0; k < SPRP_ILP; ++k) ok[k] = ok[k] && t[k];
+            sprp_multi<SPRP_ILP>(q, 7, t);
+#pragma unroll
+            for (int k = 0; k < SPRP_ILP; ++k) ok[k] = ok[k] && t[k];
+            sprp_multi<SPRP_ILP>(q, 61, t);
+#pragma unroll
+            for (int k = 0; k < SPRP_ILP; ++k) {
+                ok[k] = ok[k] && t[k];
+                if (ok[k]) {
+                    const uint64_t j = cand_index(R, v[k]);
+                    if (j != ~0ull) atomicOr(&words[j >> 5], 1u << (j & 31));
+                }
+            }
+        }
+    }
+}
+
 __global__ void k_is_safe(const uint32_t* __restrict__ n, uint64_t count, uint8_t* __restrict__ is_p,
                           uint8_t* __restrict__ is_s) {
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count;
@@ -741,6 +898,78 @@ extern "C" int rsa_safe_prime_scan(uint64_t lo, uint64_t hi, uint32_t* out, uint
     if ((rc = launch_status("rsa_safe_prime_scan(offsets)"))) return rc;
     k_scan_write<<<tail_grid, TAIL_BLOCK, 0, st>>>(R, words, ctas, offsets, out, out_cap);
     return launch_status("rsa_safe_prime_scan(write)");
+}
+
+// literal scan: chunks of MR_CHUNK odd candidates, list capacity bounded by
+// the prime density among odd n >= 10201 (< 2 / ln 10201 < 1/4)
+constexpr uint64_t MR_CHUNK = 1ull << 26;
+constexpr uint64_t MR_LIST = MR_CHUNK / 4 + 4096;
+
+static bool mr_range(uint64_t lo, uint64_t hi, uint64_t* lo_odd, uint64_t* n_odd) {
+    if (hi > (1ull << 32)) return false;
+    if (lo < 3) lo = 3;
+    *lo_odd = lo | 1;
+    *n_odd = hi > *lo_odd ? (hi - *lo_odd + 1) / 2 : 0;
+    return true;
+}
+
+extern "C" uint64_t rsa_safe_prime_scan_mr_scratch_bytes(uint64_t lo, uint64_t hi) {
+    ScanRange R;
+    uint64_t a, b;
+    if (!make_range(lo, hi, &R) || !mr_range(lo, hi, &a, &b)) return 0;
+    uint64_t ctas = scan_ctas(R);
+    if (ctas == 0) ctas = 1;
+    uint64_t words = ctas * WORDS_PER_CTA * 4, counts = ((ctas * 4 + 15) / 16) * 16;
+    return words + counts + ctas * 8 + MR_LIST * 4 + 16;
+}
+
+extern "C" int rsa_safe_prime_scan_mr(uint64_t lo, uint64_t hi, uint32_t* out, uint64_t out_cap,
+                                      uint64_t* count, void* scratch, uint64_t scratch_bytes,
+                                      void* stream) {
+    ScanRange R;
+    uint64_t lo_odd, n_odd;
+    if (!count || !make_range(lo, hi, &R) || !mr_range(lo, hi, &lo_odd, &n_odd)) return RSA_EINVAL;
+    if (scratch_bytes < rsa_safe_prime_scan_mr_scratch_bytes(lo, hi) || !scratch) return RSA_EINVAL;
+    if (out_cap && !out) return RSA_EINVAL;
+    cudaStream_t st = as_stream(stream);
+    uint64_t ctas = scan_ctas(R);
+    if (ctas == 0) {
+        cudaError_t err = cudaMemsetAsync(count, 0, sizeof(uint64_t), st);
+        if (err != cudaSuccess) { set_last_error("rsa_safe_prime_scan_mr", err); return RSA_ECUDA; }
+        return RSA_OK;
+    }
+    char* p = static_cast<char*>(scratch);
+    uint32_t* words = reinterpret_cast<uint32_t*>(p);
+    p += ctas * WORDS_PER_CTA * 4;
+    uint32_t* counts = reinterpret_cast<uint32_t*>(p);
+    p += ((ctas * 4 + 15) / 16) * 16;
+    uint64_t* offsets = reinterpret_cast<uint64_t*>(p);
+    p += ctas * 8;
+    uint32_t* list = reinterpret_cast<uint32_t*>(p);
+    p += MR_LIST * 4;
+    uint32_t* ctr = reinterpret_cast<uint32_t*>(p);
+    cudaError_t err = cudaMemsetAsync(words, 0, ctas * WORDS_PER_CTA * 4, st);
+    if (err != cudaSuccess) { set_last_error("rsa_safe_prime_scan_mr(memset)", err); return RSA_ECUDA; }
+    const unsigned grid = 148 * (16 / SPRP_ILP);
+    int rc;
+    for (uint64_t c0 = 0; c0 < n_odd; c0 += MR_CHUNK) {
+        const uint64_t c1 = n_odd - c0 < MR_CHUNK ? n_odd : c0 + MR_CHUNK;
+        if ((err = cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st)) != cudaSuccess) {
+            set_last_error("rsa_safe_prime_scan_mr(memset)", err);
+            return RSA_ECUDA;
+        }
+        k_mr_base2<<<grid, SCAN_BLOCK, 0, st>>>(R, lo_odd, c0, c1, list, ctr, words);
+        if ((rc = launch_status("rsa_safe_prime_scan_mr(base 2)"))) return rc;
+        k_mr_rest<<<grid, SCAN_BLOCK, 0, st>>>(R, list, ctr, words);
+        if ((rc = launch_status("rsa_safe_prime_scan_mr(bases 7, 61; q)"))) return rc;
+    }
+    const unsigned tail_grid = (unsigned)(ctas < 148 * 16 ? ctas : 148 * 16);
+    k_scan_counts<<<tail_grid, TAIL_BLOCK, 0, st>>>(words, ctas, counts);
+    if ((rc = launch_status("rsa_safe_prime_scan_mr(counts)"))) return rc;
+    k_scan_offsets<<<1, 1024, 0, st>>>(counts, ctas, offsets, count);
+    if ((rc = launch_status("rsa_safe_prime_scan_mr(offsets)"))) return rc;
+    k_scan_write<<<tail_grid, TAIL_BLOCK, 0, st>>>(R, words, ctas, offsets, out, out_cap);
+    return launch_status("rsa_safe_prime_scan_mr(write)");
 }
 
 extern "C" int rsa_is_safe_prime32(const uint32_t* n, uint64_t count, uint8_t* is_prime,

@@ -55,8 +55,11 @@ class StreamKey:
 # ---------------------------------------------------------------------------
 # safe primes on the device
 
-def safe_primes_u32(lo: int, hi: int, dev=None) -> torch.Tensor:
-    """Ascending safe primes in [lo, hi) (hi <= 2^32) as a uint32 device tensor."""
+def safe_primes_u32(lo: int, hi: int, dev=None, literal_mr: bool = False) -> torch.Tensor:
+    """Ascending safe primes in [lo, hi) (hi <= 2^32) as a uint32 device tensor.
+    literal_mr: run the census as BASELINE config 5 words it (Miller-Rabin
+    2, 7, 61 on every odd n and on (n-1)/2, rsa_safe_prime_scan_mr) instead of
+    the sieve + base-2 SPRP + pseudoprime-table scan; the list is the same."""
     if hi > 1 << 32:
         raise ValueError("sieve windows are limited to 2^32")
     d = _device.device(dev)
@@ -64,16 +67,17 @@ def safe_primes_u32(lo: int, hi: int, dev=None) -> torch.Tensor:
     if lo >= hi:
         return torch.empty(0, dtype=torch.uint32, device=d)
     L = _lib.load()
-    scratch_bytes = int(L.rsa_safe_prime_scan_scratch_bytes(lo, hi))
+    fn = "rsa_safe_prime_scan_mr" if literal_mr else "rsa_safe_prime_scan"
+    scratch_bytes = int(getattr(L, fn + "_scratch_bytes")(lo, hi))
     scratch = torch.empty(max(scratch_bytes, 16), dtype=torch.uint8, device=d)
     count = torch.zeros(1, dtype=torch.uint64, device=d)
     # capacity: the density of safe primes never exceeds 1 per 12 candidates
     # (+2 for 5 and 7); the 2^31..2^32 census is far below that
     cap = (hi - lo) // 12 + 4 if hi - lo < (1 << 26) else int(1.1 * SAFE_PRIME_CENSUS * (hi - lo) / (1 << 31)) + 4096
     out = torch.empty(cap, dtype=torch.uint32, device=d)
-    rc = L.rsa_safe_prime_scan(lo, hi, out.data_ptr(), cap, count.data_ptr(), scratch.data_ptr(),
-                               scratch_bytes, _device.stream(d))
-    _lib.check(rc, "rsa_safe_prime_scan")
+    rc = getattr(L, fn)(lo, hi, out.data_ptr(), cap, count.data_ptr(), scratch.data_ptr(),
+                        scratch_bytes, _device.stream(d))
+    _lib.check(rc, fn)
     n = int(count.cpu().numpy()[0])
     if n > cap:
         raise _lib.RsaCudaError(f"safe-prime scan overflow ({n} > {cap})")

@@ -35,6 +35,39 @@ def test_scan_windows(lo, hi):
     assert got == want
 
 
+def test_literal_mr_census(golden_census):
+    """BASELINE config 5 verbatim: MR (2, 7, 61) on every odd n in
+    [2^31, 2^32) and on (n-1)/2 gives the reference's census exactly."""
+    sp = paramfactory.safe_primes_u32(1 << 31, 1 << 32, literal_mr=True).cpu().numpy().view(np.uint32)
+    assert len(sp) == golden_census["safe_primes"]
+    assert sha(sp.astype("<u4")) == golden_census["sha256_u32le"]
+
+
+@pytest.mark.parametrize("lo,hi", [(2, 5000), (0, 12), (5, 8), (10_190, 10_230), (10_000, 400_000),
+                                   ((1 << 31) - 5, (1 << 31) + 5), ((1 << 32) - 1_000_000, 1 << 32),
+                                   (3037000000, 3037100000)])
+def test_literal_mr_windows(lo, hi):
+    a = paramfactory.safe_primes_u32(lo, hi, literal_mr=True).cpu().numpy().tolist()
+    b = paramfactory.safe_primes_u32(lo, hi).cpu().numpy().tolist() if hi > max(lo, 2) else []
+    assert a == b
+    want = [p for p in range(max(lo, 2), min(hi, 11)) if O.is_safe_prime(p)]
+    if hi > 11:
+        sp, _ = coracle.census(max(lo, 11), hi)
+        want += sp.tolist()
+    assert a == want
+
+
+def test_literal_mr_pseudoprime_neighbourhoods():
+    """Base-2 strong pseudoprimes (and their safe-prime partners) decided by
+    bases 7 / 61 in the literal scan, equal to the table-based scan."""
+    from test_spsp2_table import load_table
+    _, _, vals = load_table()
+    for t in vals[::23]:
+        lo, hi = max(11, t - 300), min(1 << 32, t + 300)
+        assert paramfactory.safe_primes_u32(lo, hi, literal_mr=True).cpu().numpy().tolist() == \
+            paramfactory.safe_primes_u32(lo, hi).cpu().numpy().tolist(), t
+
+
 def test_scan_pseudoprime_neighbourhoods():
     """Every candidate whose verdict the base-2 pseudoprime table decides (p or
     (p-1)/2 is a base-2 strong pseudoprime and the other half passes base 2)
