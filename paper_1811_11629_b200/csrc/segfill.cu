@@ -7,8 +7,9 @@
 //   * the message m_k = m_0 + sum_{i<=k} s_i (mod p) is a prefix sum, so each
 //     segment's contribution sum_{i in seg} s_i (mod p1, mod p2) can be formed
 //     independently and combined by an exclusive scan over the segments.
-// Three launches: k_seg_sums (per segment: jump, walk L skips, sum REDC(s) in
-// the R^-1 domain), k_seg_scan (per lane: exclusive scan of its segment sums),
+// Three stages: k_seg_sums (per segment: jump, walk L skips, sum REDC(s) in
+// the R^-1 domain), the exclusive scan of each lane's segment sums (k_seg_scan
+// for a few segments per lane, else the chunked k_seg_chunk_tot/apply pair),
 // k_seg_fill (per segment: jump again, start from m_0 + prefix, run the full
 // draw and write the outputs).  The result is bit-identical to the sequential
 // lane (same values, same stream order); the cost is one extra skip + 2 REDC
@@ -70,65 +71,12 @@ k_seg_sums(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t lanes, u
     sums[2 * t + 1] = a2;
 }
 
-// Exclusive scan over the segments of each lane (in place), mod p1 / p2:
-// one CTA per lane, warp w owns a contiguous run of segments and walks it 32
-// at a time (coalesced loads, a shuffle scan per step, a running carry); the
-// warp totals are scanned once more and added on the way out.  Modular
-// addition is associative, so the result equals the sequential scan.
+// inclusive warp scan of (v1, v2) mod (p1, p2)
 RSA_DEV void warp_scan2(uint32_t& v1, uint32_t& v2, uint32_t p1, uint32_t p2, int wl) {
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
         const uint32_t o1 = __shfl_up_sync(0xffffffffu, v1, d), o2 = __shfl_up_sync(0xffffffffu, v2, d);
         if (wl >= d) { v1 = add_mod(v1, o1, p1); v2 = add_mod(v2, o2, p2); }
-    }
-}
-
-__global__ void __launch_bounds__(1024)
-k_seg_scan_block(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t lanes, uint64_t nseg,
-                 uint32_t* __restrict__ sums) {
-    __shared__ uint32_t w1[32], w2[32];
-    const uint64_t lane = blockIdx.x;
-    const rsa_instance* ip = inst + lane / mv;
-    const uint32_t p1 = ip->p1, p2 = ip->p2;
-    const int wl = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const uint64_t per = (nseg + nw - 1) / nw;  // segments per warp
-    const uint64_t j0 = (uint64_t)wid * per, j1 = min(nseg, j0 + per);
-    // pass 1: warp totals
-    uint32_t t1 = 0, t2 = 0;
-    for (uint64_t j = j0 + wl; j < j1; j += 32) {
-        const uint64_t t = j * lanes + lane;
-        t1 = add_mod(t1, sums[2 * t], p1);
-        t2 = add_mod(t2, sums[2 * t + 1], p2);
-    }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-        t1 = add_mod(t1, __shfl_xor_sync(0xffffffffu, t1, d), p1);
-        t2 = add_mod(t2, __shfl_xor_sync(0xffffffffu, t2, d), p2);
-    }
-    if (wl == 0) { w1[wid] = t1; w2[wid] = t2; }
-    __syncthreads();
-    if (wid == 0) {  // exclusive scan of the warp totals
-        uint32_t x1 = wl < nw ? w1[wl] : 0, x2 = wl < nw ? w2[wl] : 0;
-        uint32_t y1 = x1, y2 = x2;
-        warp_scan2(y1, y2, p1, p2, wl);
-        if (wl < nw) { w1[wl] = sub_mod(y1, x1, p1); w2[wl] = sub_mod(y2, x2, p2); }
-    }
-    __syncthreads();
-    // pass 2: rewrite each run with its exclusive prefix, 32 segments per step
-    uint32_t c1 = w1[wid], c2 = w2[wid];
-    for (uint64_t base = j0; base < j1; base += 32) {
-        const uint64_t j = base + wl;
-        const bool in = j < j1;
-        const uint64_t t = j * lanes + lane;
-        const uint32_t v1 = in ? sums[2 * t] : 0, v2 = in ? sums[2 * t + 1] : 0;
-        uint32_t i1 = v1, i2 = v2;
-        warp_scan2(i1, i2, p1, p2, wl);
-        if (in) {
-            sums[2 * t] = add_mod(c1, sub_mod(i1, v1, p1), p1);
-            sums[2 * t + 1] = add_mod(c2, sub_mod(i2, v2, p2), p2);
-        }
-        c1 = add_mod(c1, __shfl_sync(0xffffffffu, i1, 31), p1);
-        c2 = add_mod(c2, __shfl_sync(0xffffffffu, i2, 31), p2);
     }
 }
 
@@ -147,6 +95,99 @@ __global__ void k_seg_scan(const rsa_instance* __restrict__ inst, uint32_t mv, u
         sums[2 * t + 1] = r2;
         r1 = add_mod(r1, v1, p1);
         r2 = add_mod(r2, v2, p2);
+    }
+}
+
+// Chunked scan for many segments per lane: chunks of SEG_CHUNK segments of
+// one lane per CTA.  Pass A: chunk totals.  Pass C: each CTA adds up the
+// totals of its lane's earlier chunks (at most a few dozen), then a block
+// scan of its own segments writes the exclusive prefixes in place.  Two
+// fully parallel launches instead of one CTA walking every segment of a lane.
+constexpr int SEG_SCAN_BLOCK = 256, SEG_PER_THREAD = 4;
+constexpr uint64_t SEG_CHUNK = (uint64_t)SEG_SCAN_BLOCK * SEG_PER_THREAD;
+
+// block-wide exclusive scan of (v1, v2) mod (p1, p2); returns the block totals
+RSA_DEV void block_excl_scan2(uint32_t& v1, uint32_t& v2, uint32_t p1, uint32_t p2,
+                              uint32_t* tot1, uint32_t* tot2) {
+    __shared__ uint32_t w1[SEG_SCAN_BLOCK / 32], w2[SEG_SCAN_BLOCK / 32];
+    const int wl = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t x1 = v1, x2 = v2;
+    warp_scan2(v1, v2, p1, p2, wl);  // inclusive within the warp
+    if (wl == 31) { w1[wid] = v1; w2[wid] = v2; }
+    __syncthreads();
+    uint32_t b1 = 0, b2 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+    for (int k = 0; k < SEG_SCAN_BLOCK / 32; ++k) {
+        if (k < wid) { b1 = add_mod(b1, w1[k], p1); b2 = add_mod(b2, w2[k], p2); }
+        a1 = add_mod(a1, w1[k], p1);
+        a2 = add_mod(a2, w2[k], p2);
+    }
+    v1 = add_mod(b1, sub_mod(v1, x1, p1), p1);
+    v2 = add_mod(b2, sub_mod(v2, x2, p2), p2);
+    *tot1 = a1;
+    *tot2 = a2;
+}
+
+__global__ void __launch_bounds__(SEG_SCAN_BLOCK)
+k_seg_chunk_tot(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t lanes, uint64_t nseg,
+                uint64_t nchunk, const uint32_t* __restrict__ sums, uint32_t* __restrict__ ctot) {
+    const uint64_t lane = blockIdx.x / nchunk, c = blockIdx.x - lane * nchunk;
+    const rsa_instance* ip = inst + lane / mv;
+    const uint32_t p1 = ip->p1, p2 = ip->p2;
+    uint32_t v1 = 0, v2 = 0;
+#pragma unroll
+    for (int i = 0; i < SEG_PER_THREAD; ++i) {
+        const uint64_t j = c * SEG_CHUNK + (uint64_t)i * SEG_SCAN_BLOCK + threadIdx.x;
+        if (j < nseg) {
+            const uint64_t t = j * lanes + lane;
+            v1 = add_mod(v1, sums[2 * t], p1);
+            v2 = add_mod(v2, sums[2 * t + 1], p2);
+        }
+    }
+    uint32_t a1, a2;
+    block_excl_scan2(v1, v2, p1, p2, &a1, &a2);
+    if (threadIdx.x == 0) { ctot[2 * blockIdx.x] = a1; ctot[2 * blockIdx.x + 1] = a2; }
+}
+
+__global__ void __launch_bounds__(SEG_SCAN_BLOCK)
+k_seg_chunk_apply(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t lanes, uint64_t nseg,
+                  uint64_t nchunk, uint32_t* __restrict__ sums, const uint32_t* __restrict__ ctot) {
+    const uint64_t lane = blockIdx.x / nchunk, c = blockIdx.x - lane * nchunk;
+    const rsa_instance* ip = inst + lane / mv;
+    const uint32_t p1 = ip->p1, p2 = ip->p2;
+    // offset of this chunk: the lane's earlier chunk totals (warp 0 adds them up)
+    __shared__ uint32_t off1, off2;
+    if (threadIdx.x < 32) {
+        uint32_t o1 = 0, o2 = 0;
+        for (uint64_t k = threadIdx.x; k < c; k += 32) {
+            o1 = add_mod(o1, ctot[2 * (lane * nchunk + k)], p1);
+            o2 = add_mod(o2, ctot[2 * (lane * nchunk + k) + 1], p2);
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            o1 = add_mod(o1, __shfl_xor_sync(0xffffffffu, o1, d), p1);
+            o2 = add_mod(o2, __shfl_xor_sync(0xffffffffu, o2, d), p2);
+        }
+        if (threadIdx.x == 0) { off1 = o1; off2 = o2; }
+    }
+    // the SEG_PER_THREAD segments of a thread are strided by the block size;
+    // scan them one stride-row at a time, carrying the row totals
+    uint32_t c1 = 0, c2 = 0;
+    __syncthreads();
+    c1 = off1;
+    c2 = off2;
+#pragma unroll
+    for (int i = 0; i < SEG_PER_THREAD; ++i) {
+        const uint64_t j = c * SEG_CHUNK + (uint64_t)i * SEG_SCAN_BLOCK + threadIdx.x;
+        const uint64_t t = j * lanes + lane;
+        uint32_t v1 = 0, v2 = 0;
+        if (j < nseg) { v1 = sums[2 * t]; v2 = sums[2 * t + 1]; }
+        uint32_t a1, a2;
+        block_excl_scan2(v1, v2, p1, p2, &a1, &a2);
+        if (j < nseg) { sums[2 * t] = add_mod(c1, v1, p1); sums[2 * t + 1] = add_mod(c2, v2, p2); }
+        c1 = add_mod(c1, a1, p1);
+        c2 = add_mod(c2, a2, p2);
+        __syncthreads();  // the block scan's shared words are reused by the next row
     }
 }
 
@@ -200,19 +241,24 @@ static void launch_seg_fill(unsigned grid, cudaStream_t st, const rsa_instance* 
         k_seg_fill<E, false, true><<<grid, 256, 0, st>>>(inst, mv, lanes, blocks, L, nseg, m1, m2, s, st0, pre, raw, f64, stride);
 }
 
+#ifndef RSA_SEG_MIN
+#define RSA_SEG_MIN 16  // shortest segment (draws); jump-ahead cost ~ 20 q63 products per segment
+#endif
 extern "C" uint64_t rsa_fill_segments(uint64_t lanes, uint64_t blocks) {
-    // enough threads to fill the chip (~2^18), segments of >= 64 draws
-    if (lanes == 0 || blocks < 128) return 1;
+    // enough threads to fill the chip (~2^18), segments of >= RSA_SEG_MIN draws
+    if (lanes == 0 || blocks < 2 * RSA_SEG_MIN) return 1;
     const uint64_t target = 1ull << 18;
     if (lanes >= target / 2) return 1;
     uint64_t nseg = target / lanes;
-    uint64_t maxseg = blocks / 64;
+    uint64_t maxseg = blocks / RSA_SEG_MIN;
     if (nseg > maxseg) nseg = maxseg;
     return nseg < 1 ? 1 : nseg;
 }
 
 extern "C" uint64_t rsa_fill_segmented_scratch_bytes(uint64_t lanes, uint64_t blocks) {
-    return lanes * sizeof(SegState) + rsa_fill_segments(lanes, blocks) * lanes * 2 * sizeof(uint32_t);
+    const uint64_t nseg = rsa_fill_segments(lanes, blocks);
+    const uint64_t nchunk = (nseg + SEG_CHUNK - 1) / SEG_CHUNK;
+    return lanes * sizeof(SegState) + (nseg + nchunk) * lanes * 2 * sizeof(uint32_t);
 }
 
 extern "C" int rsa_fill_segmented(const rsa_instance* inst, uint32_t n_inst, uint32_t mv, uint64_t blocks,
@@ -237,10 +283,12 @@ extern "C" int rsa_fill_segmented(const rsa_instance* inst, uint32_t n_inst, uin
     k_seg_sums<<<grid_for(threads, 256), 256, 0, st>>>(inst, mv, lanes, blocks, L, nseg_eff, m1, m2, s, st0, sums);
     int rc = launch_status("rsa_fill_segmented(sums)");
     if (rc) return rc;
-    if (nseg_eff >= 64) {  // long segment chains: one CTA per lane
-        unsigned tb = 32;
-        while (tb < 1024 && tb * 8 < nseg_eff) tb <<= 1;
-        k_seg_scan_block<<<(unsigned)lanes, tb, 0, st>>>(inst, mv, lanes, nseg_eff, sums);
+    if (nseg_eff >= 64) {  // long segment chains: chunked parallel scan
+        const uint64_t nchunk = (nseg_eff + SEG_CHUNK - 1) / SEG_CHUNK;
+        uint32_t* ctot = sums + 2 * nseg_eff * lanes;
+        k_seg_chunk_tot<<<(unsigned)(lanes * nchunk), SEG_SCAN_BLOCK, 0, st>>>(inst, mv, lanes, nseg_eff, nchunk, sums, ctot);
+        if ((rc = launch_status("rsa_fill_segmented(scan totals)"))) return rc;
+        k_seg_chunk_apply<<<(unsigned)(lanes * nchunk), SEG_SCAN_BLOCK, 0, st>>>(inst, mv, lanes, nseg_eff, nchunk, sums, ctot);
     } else {
         k_seg_scan<<<grid_for(lanes, 128), 128, 0, st>>>(inst, mv, lanes, nseg_eff, sums);
     }

@@ -389,7 +389,8 @@ def test_float_map_many_moduli_and_near_midpoints(golden_streams):
         assert np.array_equal(u64np(out), want), n
 
 
-@pytest.mark.parametrize("mv,blocks,e", [(1, 1 << 18, 9), (3, 40000, 5), (64, 20000, 65537), (100, 3000, 7)])
+@pytest.mark.parametrize("mv,blocks,e", [(1, 1 << 18, 9), (1, 1 << 20, 3), (3, 40000, 5), (64, 20000, 65537),
+                                         (100, 3000, 7), (2048, 100, 9)])
 def test_segmented_fill_equals_lane_fill(p0, mv, blocks, e):
     """rsa_fill_segmented (lanes split across threads: jump-ahead skip + scanned
     message sums) is bit-identical to the one-thread-per-lane rsa_fill, outputs
