@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define RSA_ABI_VERSION 2
+#define RSA_ABI_VERSION 3
 
 /* status codes */
 #define RSA_OK 0
@@ -198,11 +198,13 @@ int rsa_safe_prime_scan_mr(uint64_t lo, uint64_t hi, uint32_t* out, uint64_t out
 int rsa_is_safe_prime32(const uint32_t* n, uint64_t count, uint8_t* is_prime,
                         uint8_t* is_safe, void* stream);
 
-/* Bucket index of a sorted u32 table: index[b] = number of entries < b*2^16,
- * b = 0..65536 (RSA_SP_INDEX_LEN entries).  Lets rsa_find_pair /
- * rsa_setup_instances start their search inside one 2^16-wide bucket
- * (~90 safe primes) instead of the whole table. */
-#define RSA_SP_INDEX_LEN 65537u
+/* Bucket index of a sorted u32 table: index[b] = number of entries
+ * < b*2^RSA_SP_INDEX_SHIFT, b = 0..2^(32-RSA_SP_INDEX_SHIFT) (RSA_SP_INDEX_LEN
+ * entries).  Lets rsa_find_pair / rsa_setup_instances start their search
+ * inside one 2^12-wide bucket
+ * (~3 safe primes) instead of the whole table. */
+#define RSA_SP_INDEX_SHIFT 12u
+#define RSA_SP_INDEX_LEN ((1u << (32u - RSA_SP_INDEX_SHIFT)) + 1u)
 int rsa_safe_prime_index(const uint32_t* sp, uint64_t n_sp, uint32_t* index, void* stream);
 
 /* find_pair (paramfactory.py:195-219) for a batch of p1 values against the

@@ -54,7 +54,7 @@ class SetupConfig(ctypes.Structure):
                 ("max_steps", c_u32), ("start_step", c_u32)]
 
 
-ABI_VERSION = 2  # include/rsarand_b200.h RSA_ABI_VERSION
+ABI_VERSION = 3  # include/rsarand_b200.h RSA_ABI_VERSION
 
 # name -> (restype, argtypes); the CPU test checks this list against include/*.h
 PROTOTYPES = {

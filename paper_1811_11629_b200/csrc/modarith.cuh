@@ -108,6 +108,26 @@ RSA_DEV uint64_t skip_q63(uint64_t s, uint32_t a) {
     return (t >> 63) ? (t & 0x7FFFFFFFFFFFFFFFull) : r;
 }
 
+// floor(x / d) for d < 2^62 when the quotient is known to be < 2^50: an FP64
+// estimate (x, d, 1/d and the product each rounded once: relative error
+// < 2^-51, so the estimate is off by at most one) fixed up exactly in
+// wrapping 64-bit arithmetic; *rem = x mod d.  Stands in for the software
+// 64-bit division (~100 instructions) on the setup paths.
+RSA_DEV uint64_t div_small_q(uint64_t x, uint64_t d, uint64_t* rem) {
+    uint64_t q = __double2ull_rz(__dmul_rn(__ull2double_rn(x), __drcp_rn(__ull2double_rn(d))));
+    int64_t r = (int64_t)(x - q * d);  // true remainder +- d: within int64 since d < 2^62
+    if (r < 0) { r += (int64_t)d; --q; }
+    else if (r >= (int64_t)d) { r -= (int64_t)d; ++q; }
+    *rem = (uint64_t)r;
+    return q;
+}
+
+RSA_DEV uint64_t mod_small_q(uint64_t x, uint64_t d) {
+    uint64_t r;
+    div_small_q(x, d, &r);
+    return r;
+}
+
 // Exact x*y mod m for 64-bit operands (setup paths only).
 RSA_DEV uint64_t mulmod64(uint64_t x, uint64_t y, uint64_t m) {
     unsigned __int128 t = (unsigned __int128)x * y;

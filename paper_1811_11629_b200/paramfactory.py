@@ -5,7 +5,7 @@ paramfactory.py:24-278).
 Where the reference sieves the p1 window lazily and searches partners with
 per-candidate Miller-Rabin calls, this module keeps ONE device-resident sorted
 list of all 3,060,794 safe primes of [2^31, 2^32) (built once per device by
-the K3 scan, csrc/primes.cu) plus its 2^16-bucket index; the pair search and
+the K3 scan, csrc/primes.cu) plus its 2^12-bucket index; the pair search and
 the instance constants run in K4 (csrc/setup.cu), one thread per stream id.
 `derive_params_table` is the batch form (configs 3-5).
 """
@@ -113,13 +113,14 @@ def nth_safe_prime_in(lo: int, hi: int, k: int, dev=None) -> int:
 
 def safe_prime_index(sp: torch.Tensor) -> torch.Tensor:
     """Bucket index of a sorted device u32 table (rsa_safe_prime_index):
-    index[b] = number of entries below b*2^16, b = 0..65536."""
+    index[b] = number of entries below b*2^SP_INDEX_SHIFT, b = 0..2^(32-SP_INDEX_SHIFT)."""
     idx = torch.empty(SP_INDEX_LEN, dtype=torch.int32, device=sp.device)
     _lib.call("rsa_safe_prime_index", sp.data_ptr(), int(sp.numel()), idx.data_ptr(), _device.stream(sp.device))
     return idx
 
 
-SP_INDEX_LEN = 65537
+SP_INDEX_SHIFT = 12                          # include/rsarand_b200.h RSA_SP_INDEX_SHIFT
+SP_INDEX_LEN = (1 << (32 - SP_INDEX_SHIFT)) + 1
 
 
 class SafePrimeTable:

@@ -24,7 +24,7 @@ def test_library_builds_and_loads():
     path = _build.build()
     assert os.path.exists(path)
     lib = _lib.load()
-    assert lib.rsa_abi_version() == 2
+    assert lib.rsa_abi_version() == _lib.ABI_VERSION == 3
     assert lib.rsa_built_arch() == 100
 
 

@@ -192,7 +192,7 @@ def test_safe_prime_index_and_unindexed_search(golden_streams):
     """The bucket index matches searchsorted, and the indexed search returns
     byte-identical instances / pairs to the plain binary search (NULL index)."""
     tab = paramfactory.safe_prime_table()
-    keys = torch.arange(paramfactory.SP_INDEX_LEN, dtype=torch.int64, device=tab.sp.device) << 16
+    keys = torch.arange(paramfactory.SP_INDEX_LEN, dtype=torch.int64, device=tab.sp.device) << paramfactory.SP_INDEX_SHIFT
     want = torch.searchsorted(tab.sp.to(torch.int64), keys)
     assert torch.equal(tab.index.to(torch.int64), want)
     n = 1 << 16
