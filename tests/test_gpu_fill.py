@@ -499,3 +499,31 @@ def test_next_skip_array():
         t = torch.from_numpy(s.view(np.int64)).cuda().view(torch.uint64)
         assert np.array_equal(u64np(skipgen.next_skip_array(t, sp)), want)
     assert skipgen.next_skip_array(np.zeros(0, dtype=np.uint64), sp).size == 0
+
+
+def test_distinct_states_on_concurrent_streams(p0):
+    """Distinct states advanced concurrently on distinct CUDA streams (the
+    reentrancy promise of include/rsarand_b200.h) give the
+    same draws as one after the other: lane fill, segmented fill and host out."""
+    cases = [(4096, 64 * 4096), (1, 1 << 16), (64, 64 * 3000)]
+    want = []
+    for mv, n in cases:
+        st = R.init_vector(p0, m0=777, mv=mv)
+        want.append(u64np(R.take_floats(st, n)))
+    streams = [torch.cuda.Stream() for _ in cases]
+    outs = []
+    for (mv, n), s in zip(cases, streams):
+        with torch.cuda.stream(s):
+            st = R.init_vector(p0, m0=777, mv=mv)
+            outs.append(R.take_floats(st, n))
+    torch.cuda.synchronize()
+    for w, o in zip(want, outs):
+        assert np.array_equal(w, u64np(o))
+    # host-out takes on two streams at once
+    hosts = [torch.empty(n, dtype=torch.float64).pin_memory() for _, n in cases[:2]]
+    for (mv, n), s, h in zip(cases[:2], streams, hosts):
+        with torch.cuda.stream(s):
+            R.take_floats(R.init_vector(p0, m0=777, mv=mv), n, out=h)
+    torch.cuda.synchronize()
+    for w, h in zip(want, hosts):
+        assert np.array_equal(w, h.numpy())
