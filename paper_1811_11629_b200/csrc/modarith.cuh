@@ -128,6 +128,26 @@ RSA_DEV uint64_t mod_small_q(uint64_t x, uint64_t d) {
     return r;
 }
 
+// x*y mod n for x, y < n, 2^32 <= n < 2^64, without the software 128-bit
+// modulo: the quotient is estimated in FP64 (off by < 2^13), the residue
+// P - Qe*n is formed exactly in 128-bit integers, one more FP64 rounding of
+// residue/n brings it into (-n, n), and one conditional add finishes.
+RSA_DEV uint64_t mulmod64_fp(uint64_t x, uint64_t y, uint64_t n) {
+    const unsigned __int128 P = (unsigned __int128)x * y;
+    const double ninv = __drcp_rn(__ull2double_rn(n));
+    const double Pd = __fma_rn(__ull2double_rn((uint64_t)(P >> 64)), 0x1p64, __ull2double_rn((uint64_t)P));
+    const double qd = __dmul_rn(Pd, ninv);
+    const uint64_t qe = qd >= 0x1p64 ? ~0ull : __double2ull_rz(qd);
+    __int128 R = (__int128)(P - (unsigned __int128)qe * n);  // exact: |R| < 2^13 n
+    const double Rd = __fma_rn((double)(int64_t)(uint64_t)((unsigned __int128)R >> 64), 0x1p64,
+                               __ull2double_rn((uint64_t)R));
+    const int64_t q2 = __double2ll_rn(__dmul_rn(Rd, ninv));
+    R -= (__int128)q2 * (__int128)n;  // now |R| < n
+    if (R < 0) R += n;
+    if (R >= (__int128)n) R -= n;
+    return (uint64_t)R;
+}
+
 // Exact x*y mod m for 64-bit operands (setup paths only).
 RSA_DEV uint64_t mulmod64(uint64_t x, uint64_t y, uint64_t m) {
     unsigned __int128 t = (unsigned __int128)x * y;

@@ -83,7 +83,10 @@ RSA_DEV void build_instance(rsa_instance* o, uint32_t p1, uint32_t p2, uint32_t 
     v.flags = fast ? RSA_FLAG_FAST : 0u;
     v.skip_mode = RSA_SKIP_LCG;
     v.n = n; v.q = q;
-    v.b = mulmod64(q % n, ((q - 1) >> 1) % n, n);  // q(q-1)/2 mod n, q odd
+    // q(q-1)/2 mod n, q odd; n > 2^62 here, so both factors reduce by at most a subtraction
+    const uint64_t h = (q - 1) >> 1;
+    const uint64_t qm = q >= n ? (q - n >= n ? q % n : q - n) : q, hm = h >= n ? h % n : h;
+    v.b = n >= (1ull << 32) ? mulmod64_fp(qm, hm, n) : mulmod64(qm, hm, n);
     v.n_float = __ull2double_rn(n);
     v.n_recip = __drcp_rn(v.n_float);
     v.n_recip_lo = __dmul_rn(__fma_rn(-v.n_float, v.n_recip, 1.0), v.n_recip);
