@@ -415,11 +415,18 @@ def run_gpu(args):
     else:
         from bench_configs import run_other
         line = run_other(args, world, rank, local)
+    table = line.pop("_table", None)
     if rank == 0:
         if not args.no_cpu and world == 1:  # the CPU baseline is an N=1, rank-0 measurement
-            line["cpu_baseline"] = cpu_port_rate()
-            one = cpu_port_rate(procs=1)  # also the single-process figure
-            line["cpu_baseline"]["one_process"] = {"value": one["value"], "unit": one["unit"], "cores": 1}
+            if args.config == 2:
+                line["cpu_baseline"] = cpu_port_rate()
+                one = cpu_port_rate(procs=1)  # also the single-process figure
+                line["cpu_baseline"]["one_process"] = {"value": one["value"], "unit": one["unit"], "cores": 1}
+            else:
+                from bench_configs import cpu_baseline_for
+                cb = cpu_baseline_for(args.config, table)
+                if cb:
+                    line["cpu_baseline"] = cb
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

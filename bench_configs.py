@@ -64,6 +64,7 @@ def run_other(args, world, rank, local):
                             "peak": peak["ops_per_s"] / 1e12, "unit": "Tops/s",
                             "frac": bench.w_imad(9) * numbers / world / per / peak["ops_per_s"],
                             "traffic": bench.load_traffic("fill_c3")}
+        line["_table"] = t  # for the rank-0 CPU baseline (bench.run_gpu)
         return line
 
     if args.config == 4:
@@ -92,6 +93,7 @@ def run_other(args, world, rank, local):
                             "frac": bench.w_imad(9) * numbers / world / per / peak["ops_per_s"],
                             "traffic": bench.load_traffic("fused")}
         line["pooled_correlation"] = box["res"].pooled_correlation(total // 2)
+        line["_table"] = t  # for the rank-0 CPU baseline (bench.run_gpu)
         return line
 
     if args.config == 1:
@@ -231,3 +233,111 @@ def literal_mr_scan(args, lo, hi, dev, want_count):
                          "algorithmic_products_per_candidate": 55.5},
             "note": "literal MR(2,7,61) census (no sieve, no pseudoprime table); the production scan "
                     "(phases.scan_ms) returns the same list"}
+
+
+# ---------------------------------------------------------------------------
+# CPU baselines per configuration (rank 0, N = 1, bounded samples): the
+# reference's algorithm restated in oracle/ (test infrastructure), timed on
+# the box's host cores the way each configuration's workload runs.
+
+def _cpu_cfg1(args):
+    """Scalar stream (Mv = 1): the rsacore per-draw path in Python ints."""
+    import time
+    from oracle import rsa_oracle as O
+    P, count = args
+    t = time.perf_counter()
+    O.scalar_raws(P, count)
+    return count, time.perf_counter() - t
+
+
+def _cpu_cfg3(args):
+    """One config-3 instance: the numpy lockstep port at Mv = 64, e = 9."""
+    import time
+    from oracle import rsa_oracle as O
+    P, blocks = args
+    st = O.init(P, m0=0, s0=1, mv=64)
+    m1, m2, s = st.m1.copy(), st.m2.copy(), st.s.copy()
+    t = time.perf_counter()
+    for _ in range(blocks):
+        raw, m1, m2, s = O.block_raw(m1, m2, s, P)
+        O.floats_from_raw(raw, P)
+    return blocks * 64, time.perf_counter() - t
+
+
+def _cpu_cfg4(args):
+    """Config-4 instances: the C restatement draws each Mv = 1 stream, the
+    numpy restatement of the A13 statistics reduces them."""
+    import time
+    import numpy as np
+    from oracle import coracle
+    from oracle import rsa_oracle as O
+    plist, N = args
+    one = lambda v: np.array([v], dtype=np.uint64)
+    t = time.perf_counter()
+    rows = []
+    for (p1, p2, a) in plist:
+        _, f = coracle.fill(coracle.params(p1, p2, 9, a), one(0), one(0), one(1), N, raw=False)
+        rows.append(f.reshape(-1))
+    O.fused_reference(np.stack(rows))
+    return len(plist) * N, time.perf_counter() - t
+
+
+def _cpu_cfg5(args):
+    """A window of the census: the C restatement of the segmented sieve."""
+    import time
+    from oracle import coracle
+    lo, hi = args
+    t = time.perf_counter()
+    coracle.census(lo, hi)
+    return (hi - lo) // 2, time.perf_counter() - t
+
+
+def cpu_baseline_for(config: int, table=None) -> dict | None:
+    """cpu_baseline object for bench.py --config N (N != 2; config 2 uses
+    bench.cpu_port_rate).  `table`: the derived InstanceTable of the run."""
+    import multiprocessing as mp
+    import os
+    from oracle import rsa_oracle as O
+    procs = os.cpu_count() or 1
+    with open(os.path.join(bench.ROOT, "tests", "golden", "regression.json")) as fh:
+        import json
+        P0 = O.from_fields(json.load(fh)["params"])
+    if config == 1:
+        n = 1 << 17
+        draws, wall = _cpu_cfg1((P0, n))
+        return {"value": draws / wall / 1e9, "unit": "Gnumbers/s", "cores": 1, "kind": "port",
+                "sample": f"{n} scalar draws of stream 0 (oracle.scalar_raws: rsacore's per-draw path in "
+                          f"Python ints, rsacore.py:236-258), one process"}
+    if config == 3:
+        plist = [table.params(j) for j in range(procs)]
+        jobs = [(O.Params(p.p1, p.p2, 9, p.skip.a), 400) for p in plist]
+        with mp.get_context("fork").Pool(procs) as pool:
+            res = pool.map(_cpu_cfg3, jobs)
+        return {"value": sum(d for d, _ in res) / max(w for _, w in res) / 1e9, "unit": "Gnumbers/s",
+                "cores": procs, "kind": "port",
+                "sample": f"{procs} config-3 instances (ids 0..{procs - 1}), one per process, 400 blocks of "
+                          f"Mv = 64 each (numpy lockstep port of vecgen, e = 9)"}
+    if config == 4:
+        per = 4
+        plist = [(table.params(j).p1, table.params(j).p2, table.params(j).skip.a) for j in range(per * procs)]
+        N = 1 << 16
+        jobs = [(plist[per * k:per * k + per], N) for k in range(procs)]
+        with mp.get_context("fork").Pool(procs) as pool:
+            res = pool.map(_cpu_cfg4, jobs)
+        return {"value": sum(d for d, _ in res) / max(w for _, w in res) / 1e9, "unit": "Gnumbers/s",
+                "cores": procs, "kind": "port",
+                "sample": f"{per * procs} config-4 instances x {N} draws, {per} per process (C restatement "
+                          f"draws + numpy A13 statistics)"}
+    if config == 5:
+        span = 1 << 27
+        n5 = min(procs, (1 << 31) // span)  # disjoint windows inside [2^31, 2^32)
+        jobs = [((1 << 31) + k * span, (1 << 31) + (k + 1) * span) for k in range(n5)]
+        procs = n5
+        with mp.get_context("fork").Pool(procs) as pool:
+            res = pool.map(_cpu_cfg5, jobs)
+        return {"value": sum(d for d, _ in res) / max(w for _, w in res) / 1e9, "unit": "Gcandidates/s",
+                "cores": procs, "kind": "port",
+                "sample": f"safe-prime census of {procs} disjoint 2^27-wide windows from 2^31, one per "
+                          f"process (C restatement of the reference's segmented sieve, "
+                          f"paramfactory.py:85-130; faster than the reference's numpy sieve)"}
+    return None
