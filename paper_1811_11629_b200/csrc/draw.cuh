@@ -109,10 +109,19 @@ RSA_DEV uint32_t pow_e(uint32_t x, uint32_t e, uint32_t p, uint32_t pinv) {
 // sum is < 2 p1^2 < 2^64 and its REDC lies in (-p1, 2^32) < 2 p1, so one
 // conditional add or subtract makes h canonical.
 template <uint32_t E, bool GF = false>
+RSA_DEV void draw_tail(const FastInst& P, const Lane& L, uint32_t& h, uint32_t& c2);
+
+template <uint32_t E, bool GF = false>
 RSA_DEV void draw_fast_hc(const FastInst& P, Lane& L, uint32_t& h, uint32_t& c2) {
     L.s = skip_q63(L.s, P.a);
     L.x1 = msg_add(L.x1, L.s, P.p1, P.p1_inv);
     L.x2 = msg_add(L.x2, L.s, P.p2, P.p2_inv);
+    draw_tail<E, GF>(P, L, h, c2);
+}
+
+// The draw after its message step: two modpows, the p2 correction and Garner.
+template <uint32_t E, bool GF>
+RSA_DEV void draw_tail(const FastInst& P, const Lane& L, uint32_t& h, uint32_t& c2) {
     uint32_t y1 = pow_e<E>(L.x1, P.e, P.p1, P.p1_inv);   // m1^e R^-(2e-1)
     uint32_t y2 = pow_e<E>(L.x2, P.e, P.p2, P.p2_inv);
     c2 = mont_mul(y2, P.k2, P.p2, P.p2_inv);             // m2^e mod p2

@@ -224,6 +224,135 @@ k_seg_fill(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t lanes, u
     }
 }
 
+// ---- K1p: few lanes, moderate draw counts, one thread per draw ---------------
+//
+// For take sizes where even 16-draw segments leave the lane chains latency
+// bound (the scalar stream's 2^20 draws), the message recurrence is cut at
+// every draw instead: pass 1 walks the skip in 32-draw segments (one thread
+// each, jump-started like K1s) and stores every draw's message increment
+// REDC(s) mod p1, p2, the segments' in-CTA exclusive prefix and the CTA
+// totals; pass 2 runs one thread per draw: a warp-wide inclusive scan of the
+// increments within its segment, plus the segment and CTA prefixes, gives the
+// draw's message, and the draw itself (chain, Garner, float map) is fully
+// parallel.  Two launches instead of K1s's four; bit-identical results.
+constexpr int PD_SEG = 16;     // draws per pass-1 segment (one thread each)
+constexpr int PD_DPT = 2;      // consecutive draws per pass-2 thread
+constexpr int PD_BLOCK = 256;  // threads per CTA in both passes
+constexpr int PD_CTA2 = PD_BLOCK * PD_DPT;  // draws per pass-2 CTA
+static_assert((PD_BLOCK * PD_SEG) % PD_CTA2 == 0 && (32 * PD_DPT) % PD_SEG == 0,
+              "a pass-2 CTA lies inside one pass-1 CTA; a warp starts on a segment boundary");
+
+struct PdLane {
+    uint64_t m1, m2, s_end;  // initial residues (snapshot), skip after the last draw
+};
+
+// pass 1: CTA (lane, c) covers segments [c*PD_BLOCK, (c+1)*PD_BLOCK) of lane
+__global__ void __launch_bounds__(PD_BLOCK)
+k_pd_skips(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t blocks, uint64_t nseg,
+           uint64_t cta_per_lane, const uint64_t* __restrict__ m1, const uint64_t* __restrict__ m2,
+           const uint64_t* __restrict__ s, uint2* __restrict__ inc, uint2* __restrict__ segpre,
+           uint2* __restrict__ ctot, PdLane* __restrict__ snap) {
+    const uint64_t lane = blockIdx.x / cta_per_lane, c = blockIdx.x - lane * cta_per_lane;
+    const uint64_t j = c * PD_BLOCK + threadIdx.x;
+    const FastInst P = load_fast(inst + lane / mv);
+    uint32_t a1 = 0, a2 = 0;
+    if (j < nseg) {
+        const uint64_t k0 = j * PD_SEG, len = min((uint64_t)PD_SEG, blocks - k0);
+        uint64_t sk = seg_start(s[lane], pow_q63(P.a, PD_SEG), j);
+        uint2* out = inc + lane * blocks + k0;
+        for (uint64_t k = 0; k < len; ++k) {
+            sk = skip_q63(sk, P.a);
+            const uint32_t r1 = mont_redc(sk, P.p1, P.p1_inv), r2 = mont_redc(sk, P.p2, P.p2_inv);
+            out[k] = make_uint2(r1, r2);
+            a1 = add_mod(a1, r1, P.p1);
+            a2 = add_mod(a2, r2, P.p2);
+        }
+        if (j == nseg - 1) snap[lane] = PdLane{m1[lane], m2[lane], sk};
+    }
+    uint32_t t1, t2;
+    block_excl_scan2(a1, a2, P.p1, P.p2, &t1, &t2);
+    if (j < nseg) segpre[lane * nseg + j] = make_uint2(a1, a2);
+    if (threadIdx.x == 0) ctot[blockIdx.x] = make_uint2(t1, t2);
+}
+
+// pass 2: CTA (lane, b) covers draws [b*PD_CTA2, (b+1)*PD_CTA2) of lane,
+// PD_DPT consecutive draws per thread; warp w starts on pass-1 segment
+// (b*PD_CTA2 + w*32*PD_DPT) / PD_SEG
+template <uint32_t E, bool RAW, bool F64>
+__global__ void __launch_bounds__(PD_BLOCK)
+k_pd_draws(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t blocks, uint64_t nseg,
+           uint64_t cta1_per_lane, uint64_t cta_per_lane, const uint2* __restrict__ inc,
+           const uint2* __restrict__ segpre, const uint2* __restrict__ ctot, const PdLane* __restrict__ snap,
+           uint64_t* __restrict__ m1, uint64_t* __restrict__ m2, uint64_t* __restrict__ s,
+           uint64_t* __restrict__ raw, double* __restrict__ f64, uint64_t inst_stride) {
+    __shared__ uint32_t off1, off2;
+    const uint64_t lane = blockIdx.x / cta_per_lane, b = blockIdx.x - lane * cta_per_lane;
+    const uint64_t i = lane / mv;
+    const uint32_t g = (uint32_t)(lane - i * mv);
+    const FastInst P = load_fast(inst + i);
+    const int wl = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint64_t d0 = b * PD_CTA2 + (uint64_t)threadIdx.x * PD_DPT;  // this thread's first draw
+    if (threadIdx.x < 32) {  // the lane's pass-1 CTA totals before this CTA's pass-1 CTA
+        const uint64_t c1 = (b * PD_CTA2 / PD_SEG) / PD_BLOCK;
+        uint32_t o1 = 0, o2 = 0;
+        for (uint64_t k = threadIdx.x; k < c1; k += 32) {
+            const uint2 v = ctot[lane * cta1_per_lane + k];
+            o1 = add_mod(o1, v.x, P.p1);
+            o2 = add_mod(o2, v.y, P.p2);
+        }
+#pragma unroll
+        for (int dd = 16; dd > 0; dd >>= 1) {
+            o1 = add_mod(o1, __shfl_xor_sync(0xffffffffu, o1, dd), P.p1);
+            o2 = add_mod(o2, __shfl_xor_sync(0xffffffffu, o2, dd), P.p2);
+        }
+        if (threadIdx.x == 0) { off1 = o1; off2 = o2; }
+    }
+    // this thread's increments (past the end: zero) and their running sums
+    uint32_t q1[PD_DPT], q2[PD_DPT];
+    uint32_t t1 = 0, t2 = 0;
+#pragma unroll
+    for (int k = 0; k < PD_DPT; ++k) {
+        const uint2 v = d0 + k < blocks ? inc[lane * blocks + d0 + k] : make_uint2(0u, 0u);
+        t1 = add_mod(t1, v.x, P.p1);
+        t2 = add_mod(t2, v.y, P.p2);
+        q1[k] = t1;
+        q2[k] = t2;
+    }
+    uint32_t e1 = t1, e2 = t2;
+    warp_scan2(e1, e2, P.p1, P.p2, wl);  // inclusive over the warp's threads
+    e1 = sub_mod(e1, t1, P.p1);          // exclusive: the warp's draws before this thread
+    e2 = sub_mod(e2, t2, P.p2);
+    __syncthreads();
+    if (d0 >= blocks) return;
+    const PdLane z = snap[lane];
+    const uint2 sp = segpre[lane * nseg + (b * PD_CTA2 + (uint64_t)wid * 32 * PD_DPT) / PD_SEG];
+    // message before this thread's draws: x0 + pass-1 CTA offset + segment prefix + warp prefix
+    const uint32_t b1 = add_mod(add_mod(add_mod(mont_redc(z.m1, P.p1, P.p1_inv), off1, P.p1), sp.x, P.p1), e1, P.p1);
+    const uint32_t b2 = add_mod(add_mod(add_mod(mont_redc(z.m2, P.p2, P.p2_inv), off2, P.p2), sp.y, P.p2), e2, P.p2);
+    const uint64_t o = i * inst_stride + d0 * mv + g;
+    with_garner(P, [&](auto gf) {
+        constexpr bool GF = decltype(gf)::value;
+#pragma unroll
+        for (int k = 0; k < PD_DPT; ++k) {
+            if (d0 + k >= blocks) break;
+            Lane L;
+            L.s = 0;  // the skip is folded into the increments by pass 1
+            L.x1 = add_mod(b1, q1[k], P.p1);
+            L.x2 = add_mod(b2, q2[k], P.p2);
+            uint32_t h, c2;
+            draw_tail<E, GF>(P, L, h, c2);
+            const uint64_t c = (uint64_t)h * P.p2 + c2;
+            if constexpr (RAW) raw[o + (uint64_t)k * mv] = c;
+            if constexpr (F64) f64[o + (uint64_t)k * mv] = to_unit(c, P.n_float, P.n_recip, P.n_recip_lo);
+            if (d0 + k == blocks - 1) {  // the lane's final state
+                m1[lane] = lane_m1(P, L);
+                m2[lane] = lane_m2(P, L);
+                s[lane] = z.s_end;
+            }
+        }
+    });
+}
+
 }  // namespace rsa
 
 using namespace rsa;
@@ -255,7 +384,48 @@ extern "C" uint64_t rsa_fill_segments(uint64_t lanes, uint64_t blocks) {
     return nseg < 1 ? 1 : nseg;
 }
 
+// K1p (one thread per draw) for lanes x blocks up to PD_MAX draws; its
+// scratch holds 8 bytes per draw
+#ifndef RSA_PD_MAX
+#define RSA_PD_MAX (1ull << 23)
+#endif
+static bool use_pd(uint64_t lanes, uint64_t blocks) {
+    return blocks >= 4 * PD_SEG && lanes * blocks <= RSA_PD_MAX && rsa_fill_segments(lanes, blocks) > 1;
+}
+
+struct PdLayout {
+    uint64_t nseg, cta1, cta2, inc, segpre, ctot, snap, bytes;  // offsets in bytes
+};
+static PdLayout pd_layout(uint64_t lanes, uint64_t blocks) {
+    PdLayout Lo;
+    Lo.nseg = (blocks + PD_SEG - 1) / PD_SEG;
+    Lo.cta1 = (Lo.nseg + PD_BLOCK - 1) / PD_BLOCK;
+    Lo.cta2 = (blocks + PD_CTA2 - 1) / PD_CTA2;
+    Lo.inc = 0;
+    Lo.segpre = Lo.inc + lanes * blocks * 8;
+    Lo.ctot = Lo.segpre + lanes * Lo.nseg * 8;
+    Lo.snap = Lo.ctot + lanes * Lo.cta1 * 8;
+    Lo.bytes = Lo.snap + lanes * sizeof(PdLane);
+    return Lo;
+}
+
+template <uint32_t E>
+static void launch_pd(unsigned grid, cudaStream_t st, const rsa_instance* inst, uint32_t mv, uint64_t blocks,
+                      const PdLayout& Lo, const char* sc, uint64_t* m1, uint64_t* m2, uint64_t* s,
+                      uint64_t* raw, double* f64, uint64_t stride) {
+    const uint2* inc = reinterpret_cast<const uint2*>(sc + Lo.inc);
+    const uint2* pre = reinterpret_cast<const uint2*>(sc + Lo.segpre);
+    const uint2* tot = reinterpret_cast<const uint2*>(sc + Lo.ctot);
+    const PdLane* snap = reinterpret_cast<const PdLane*>(sc + Lo.snap);
+#define RSA_PD(R, F) k_pd_draws<E, R, F><<<grid, PD_BLOCK, 0, st>>>(inst, mv, blocks, Lo.nseg, Lo.cta1, Lo.cta2, inc, pre, tot, snap, m1, m2, s, raw, f64, stride)
+    if (raw && f64) RSA_PD(true, true);
+    else if (raw) RSA_PD(true, false);
+    else RSA_PD(false, true);
+#undef RSA_PD
+}
+
 extern "C" uint64_t rsa_fill_segmented_scratch_bytes(uint64_t lanes, uint64_t blocks) {
+    if (use_pd(lanes, blocks)) return pd_layout(lanes, blocks).bytes;
     const uint64_t nseg = rsa_fill_segments(lanes, blocks);
     const uint64_t nchunk = (nseg + SEG_CHUNK - 1) / SEG_CHUNK;
     return lanes * sizeof(SegState) + (nseg + nchunk) * lanes * 2 * sizeof(uint32_t);
@@ -273,16 +443,36 @@ extern "C" int rsa_fill_segmented(const rsa_instance* inst, uint32_t n_inst, uin
     if (!raw_out && !f64_out) return RSA_EINVAL;
     const uint64_t nseg = rsa_fill_segments(lanes, blocks);
     if (!scratch || scratch_bytes < rsa_fill_segmented_scratch_bytes(lanes, blocks)) return RSA_EINVAL;
+    cudaStream_t st = as_stream(stream);
+    int rc;
+    if (use_pd(lanes, blocks)) {  // K1p: one thread per draw, two launches
+        const PdLayout Lo = pd_layout(lanes, blocks);
+        char* sc = static_cast<char*>(scratch);
+        if (!grid_fits(lanes * Lo.cta1 * PD_BLOCK, PD_BLOCK) || !grid_fits(lanes * Lo.cta2 * PD_BLOCK, PD_BLOCK))
+            return RSA_EINVAL;
+        k_pd_skips<<<(unsigned)(lanes * Lo.cta1), PD_BLOCK, 0, st>>>(
+            inst, mv, blocks, Lo.nseg, Lo.cta1, m1, m2, s, reinterpret_cast<uint2*>(sc + Lo.inc),
+            reinterpret_cast<uint2*>(sc + Lo.segpre), reinterpret_cast<uint2*>(sc + Lo.ctot),
+            reinterpret_cast<PdLane*>(sc + Lo.snap));
+        if ((rc = launch_status("rsa_fill_segmented(per-draw skips)"))) return rc;
+        const unsigned g2 = (unsigned)(lanes * Lo.cta2);
+        switch (e) {
+            case 3: launch_pd<3>(g2, st, inst, mv, blocks, Lo, sc, m1, m2, s, raw_out, f64_out, inst_stride); break;
+            case 5: launch_pd<5>(g2, st, inst, mv, blocks, Lo, sc, m1, m2, s, raw_out, f64_out, inst_stride); break;
+            case 9: launch_pd<9>(g2, st, inst, mv, blocks, Lo, sc, m1, m2, s, raw_out, f64_out, inst_stride); break;
+            case 17: launch_pd<17>(g2, st, inst, mv, blocks, Lo, sc, m1, m2, s, raw_out, f64_out, inst_stride); break;
+            default: launch_pd<0>(g2, st, inst, mv, blocks, Lo, sc, m1, m2, s, raw_out, f64_out, inst_stride); break;
+        }
+        return launch_status("rsa_fill_segmented(per-draw fill)");
+    }
     const uint64_t L = (blocks + nseg - 1) / nseg;
     const uint64_t nseg_eff = (blocks + L - 1) / L;
     SegState* st0 = static_cast<SegState*>(scratch);
     uint32_t* sums = reinterpret_cast<uint32_t*>(st0 + lanes);
-    cudaStream_t st = as_stream(stream);
     const uint64_t threads = lanes * nseg_eff;
     if (!grid_fits(threads, 256)) return RSA_EINVAL;
     k_seg_sums<<<grid_for(threads, 256), 256, 0, st>>>(inst, mv, lanes, blocks, L, nseg_eff, m1, m2, s, st0, sums);
-    int rc = launch_status("rsa_fill_segmented(sums)");
-    if (rc) return rc;
+    if ((rc = launch_status("rsa_fill_segmented(sums)"))) return rc;
     if (nseg_eff >= 64) {  // long segment chains: chunked parallel scan
         const uint64_t nchunk = (nseg_eff + SEG_CHUNK - 1) / SEG_CHUNK;
         uint32_t* ctot = sums + 2 * nseg_eff * lanes;

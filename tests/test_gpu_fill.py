@@ -389,8 +389,10 @@ def test_float_map_many_moduli_and_near_midpoints(golden_streams):
         assert np.array_equal(u64np(out), want), n
 
 
+# lanes x blocks <= 2^23 take K1p (one thread per draw), larger ones K1s (segments)
 @pytest.mark.parametrize("mv,blocks,e", [(1, 1 << 18, 9), (1, 1 << 20, 3), (3, 40000, 5), (64, 20000, 65537),
-                                         (100, 3000, 7), (2048, 100, 9)])
+                                         (100, 3000, 7), (2048, 100, 9), (1, 70, 17),
+                                         (64, (1 << 17) + 5, 9), (8, (1 << 20) + 3, 5), (1, (1 << 23) + 7, 3)])
 def test_segmented_fill_equals_lane_fill(p0, mv, blocks, e):
     """rsa_fill_segmented (lanes split across threads: jump-ahead skip + scanned
     message sums) is bit-identical to the one-thread-per-lane rsa_fill, outputs
@@ -454,7 +456,7 @@ def test_vector_equals_interleaved_scalar_streams(p0, mv):
     assert np.array_equal(got, np.array(lanes).T.reshape(-1))
 
 
-@pytest.mark.parametrize("mv,blocks,stride_pad", [(1, 20000, 0), (5, 4000, 3), (64, 9000, 16)])
+@pytest.mark.parametrize("mv,blocks,stride_pad", [(1, 20000, 0), (5, 4000, 3), (64, 9000, 16), (64, 40000, 2)])
 def test_segmented_multi_instance(golden_streams, mv, blocks, stride_pad):
     """rsa_fill_segmented with n_inst > 1 (instance-major rows, padded
     strides) equals rsa_fill on the same lanes, outputs and final state."""
