@@ -165,12 +165,19 @@ RSA_DEV uint64_t powmod64(uint64_t b, uint64_t e, uint64_t m) {
     return r;
 }
 
-// x*y mod (2^63-25) for x, y < 2^63 by two folds of 2^63 == 25.
+// x*y mod (2^63-25) for x, y < 2^63 by folds of 2^64 == 50 (mod q): x*y =
+// hi 2^64 + lo == lo + 50 hi < 2^69; folding that once more leaves < 2^64 +
+// 1600, a third fold (+50 on a carry) < 2^64 = 2q + 50, so at most two
+// subtractions of q remain.  ~24 instructions where the 2^63 fold of the
+// full 128-bit product took ~40 (jump-ahead and lane-seed paths).
 RSA_DEV uint64_t mulmod_q63(uint64_t x, uint64_t y) {
-    unsigned __int128 t = (unsigned __int128)x * y;            // < 2^126
-    unsigned __int128 u = (t & 0x7FFFFFFFFFFFFFFFull) + (t >> 63) * 25u;  // < 2^68
-    uint64_t v = (uint64_t)(u & 0x7FFFFFFFFFFFFFFFull) + (uint64_t)(u >> 63) * 25u;  // < 2^63+2^11
-    return v >= Q63 ? v - Q63 : v;
+    const uint64_t lo = x * y, hi = __umul64hi(x, y);          // hi < 2^62
+    const unsigned __int128 v = (unsigned __int128)hi * 50u + lo;  // < 2^69
+    const unsigned __int128 w = (unsigned __int128)(uint64_t)(v >> 64) * 50u + (uint64_t)v;  // < 2^64 + 1600
+    uint64_t r = (uint64_t)w + ((w >> 64) ? 50u : 0u);
+    if (r >= Q63) r -= Q63;
+    if (r >= Q63) r -= Q63;
+    return r;
 }
 
 // Generic skip update for any prime q with a*a <= q: the reference Schrage
