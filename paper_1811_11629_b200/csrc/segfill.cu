@@ -236,7 +236,7 @@ k_seg_fill(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t lanes, u
 // draw's message, and the draw itself (chain, Garner, float map) is fully
 // parallel.  Two launches instead of K1s's four; bit-identical results.
 constexpr int PD_SEG = 16;     // draws per pass-1 segment (one thread each)
-constexpr int PD_DPT = 2;      // consecutive draws per pass-2 thread
+constexpr int PD_DPT = 4;      // consecutive draws per pass-2 thread
 constexpr int PD_BLOCK = 256;  // threads per CTA in both passes
 constexpr int PD_CTA2 = PD_BLOCK * PD_DPT;  // draws per pass-2 CTA
 static_assert((PD_BLOCK * PD_SEG) % PD_CTA2 == 0 && (32 * PD_DPT) % PD_SEG == 0,
