@@ -76,6 +76,25 @@ def test_argument_errors_need_no_gpu():
     assert lib.rsa_safe_prime_scan_scratch_bytes(1 << 31, 1 << 32) > 0
 
 
+def test_segmented_sizing_needs_no_gpu():
+    """rsa_fill_segments / rsa_fill_segmented_scratch_bytes (host-only): no
+    split for lane counts that fill the chip or runs too short to split; the
+    one-thread-per-draw regime (K1p, up to 2^23 draws) needs 8 bytes per draw
+    plus small per-segment tables; beyond it the segment regime (K1s) needs
+    only per-segment sums."""
+    lib = _lib.load()
+    assert lib.rsa_fill_segments(1 << 17, 1 << 20) == 1      # lanes fill the chip
+    assert lib.rsa_fill_segments(1, 31) == 1                 # too short to split
+    assert lib.rsa_fill_segments(1, 1 << 20) > 1
+    k1p = lib.rsa_fill_segmented_scratch_bytes(1, 1 << 20)
+    assert 8 << 20 <= k1p < (9 << 20)
+    k1s = lib.rsa_fill_segmented_scratch_bytes(1, 1 << 24)   # > 2^23 draws: K1s
+    assert 0 < k1s < (1 << 22)
+    assert lib.rsa_fill_segmented_scratch_bytes(64, 1 << 17) >= 8 << 23  # 2^23 draws: still K1p
+    assert lib.rsa_safe_prime_scan_mr_scratch_bytes(0, (1 << 32) + 1) == 0
+    assert lib.rsa_safe_prime_scan_mr_scratch_bytes(1 << 31, 1 << 32) > lib.rsa_safe_prime_scan_scratch_bytes(1 << 31, 1 << 32) // 8
+
+
 def test_c_abi_example_compiles(tmp_path):
     """examples/c_abi_stream0.c (the hot path through the C ABI alone) builds
     against include/rsarand_b200.h and links against the library."""
