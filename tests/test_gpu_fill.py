@@ -529,3 +529,28 @@ def test_distinct_states_on_concurrent_streams(p0):
     torch.cuda.synchronize()
     for w, h in zip(want, hosts):
         assert np.array_equal(w, h.numpy())
+
+
+@pytest.mark.parametrize("mv,blocks", [(1, 70), (1, 4099), (3, 1000), (64, 1 << 13), (1, (1 << 23) + 9)])
+def test_segmented_fill_stays_inside_its_buffers(p0, mv, blocks):
+    """Guard bands around the scratch and the output (compute-sanitizer is
+    not available on this pool): rsa_fill_segmented writes exactly its
+    outputs and at most rsa_fill_segmented_scratch_bytes of scratch, in both
+    the per-draw (K1p) and the segment (K1s) regimes."""
+    from paper_1811_11629_b200 import _device
+    d = torch.device("cuda")
+    lib = _lib.load()
+    inst = rsacore.device_instance(p0, d)
+    m1, m2, s = vecgen._init_lanes(inst, 1, mv, 31337, 1, d)
+    nb = int(lib.rsa_fill_segmented_scratch_bytes(mv, blocks))
+    G = 4096
+    sc = torch.full((nb + 2 * G,), 0xA5, dtype=torch.uint8, device=d)
+    n = blocks * mv
+    f = torch.full((n + 2 * G,), -7.0, dtype=torch.float64, device=d)
+    _lib.call("rsa_fill_segmented", inst.data_ptr(), 1, mv, blocks, p0.e, _lib.RSA_FLAG_FAST,
+              m1.data_ptr(), m2.data_ptr(), s.data_ptr(), None, f[G:].data_ptr(), n,
+              sc[G:].data_ptr(), nb, _device.stream(d))
+    torch.cuda.synchronize()
+    assert bool((sc[:G] == 0xA5).all()) and bool((sc[G + nb:] == 0xA5).all())
+    assert bool((f[:G] == -7.0).all()) and bool((f[G + n:] == -7.0).all())
+    assert bool((f[G:G + n] >= 0).all()) and bool((f[G:G + n] < 1).all())

@@ -237,3 +237,55 @@ def test_stream_indices_both_index_space_paths(n_a, golden_streams):
         ordinal, ai = paramfactory.stream_indices(paramfactory.StreamKey(seed, first + j), n_a)
         assert int(rec[j]["a"]) == table[ai]
         assert int(rec[j]["p1"]) == int(sp[(ordinal + int(steps[j])) % paramfactory.K_P1])
+
+
+@pytest.mark.parametrize("fn", ["rsa_safe_prime_scan", "rsa_safe_prime_scan_mr"])
+@pytest.mark.parametrize("lo,hi", [(2, 70_000), ((1 << 31) + 1, (1 << 31) + (1 << 26) + 7)])
+def test_scans_stay_inside_their_buffers(fn, lo, hi):
+    """Guard bands around scratch and output (no compute-sanitizer on this
+    pool): each scan writes only its outputs and declared scratch."""
+    from paper_1811_11629_b200 import _device
+    L = _lib.load()
+    d = torch.device("cuda")
+    nb = int(getattr(L, fn + "_scratch_bytes")(lo, hi))
+    G = 4096
+    sc = torch.full((nb + 2 * G,), 0x5A, dtype=torch.uint8, device=d)
+    want, _ = coracle.census(max(lo, 11), hi)
+    want = [p for p in range(max(lo, 2), min(hi, 11)) if O.is_safe_prime(p)] + want.tolist()
+    cap = len(want)
+    out = torch.full((cap + 2 * G,), 7, dtype=torch.int32, device=d)
+    cnt = torch.zeros(1, dtype=torch.int64, device=d)
+    rc = getattr(L, fn)(lo, hi, out[G:].data_ptr(), cap, cnt.data_ptr(), sc[G:].data_ptr(), nb, _device.stream(d))
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == cap
+    assert out[G:G + cap].cpu().numpy().view(np.uint32).tolist() == want
+    assert bool((out[:G] == 7).all()) and bool((out[G + cap:] == 7).all())
+    assert bool((sc[:G] == 0x5A).all()) and bool((sc[G + nb:] == 0x5A).all())
+
+
+def test_setup_writes_only_found_records():
+    """k_setup stages records in shared memory and writes them as 16-byte
+    words: records of ids it did not derive, and bytes past the table, stay
+    untouched."""
+    from paper_1811_11629_b200 import _device
+    tab = paramfactory.safe_prime_table()
+    d = tab.sp.device
+    n = 1000
+    cfg = paramfactory._setup_config(paramfactory.DEFAULT_MASTER_SEED, 61640, 9,
+                                     len(paramfactory.MULTIPLIER_TABLE), 0)
+    cfg.max_steps = 1  # ids whose first p1 has no partner stay NotFound (e.g. 61644)
+    mult = tab.mult_table(tuple(paramfactory.MULTIPLIER_TABLE))
+    G = 64
+    inst = torch.full(((n + 2 * G), 128), 0xC3, dtype=torch.uint8, device=d)
+    st = torch.empty(n, dtype=torch.int32, device=d)
+    _lib.call("rsa_setup_instances", cfg, n, mult.data_ptr(), tab.sp.data_ptr(), tab.n_sp,
+              tab.index.data_ptr(), tab.sp.data_ptr(), tab.n_p1, inst[G:].data_ptr(), st.data_ptr(), None,
+              _device.stream(d))
+    torch.cuda.synchronize()
+    s = st.cpu().numpy()
+    rec = inst[G:G + n].cpu().numpy()
+    assert (s != 0).any() and (s == 0).any()
+    assert (rec[s != 0] == 0xC3).all()
+    assert not (rec[s == 0] == 0xC3).all(axis=1).any()
+    assert bool((inst[:G] == 0xC3).all()) and bool((inst[G + n:] == 0xC3).all())

@@ -19,6 +19,11 @@ R.rsacore.take_raws(sc, p, 5)
 t = R.derive_params_table(R.DEFAULT_MASTER_SEED, 0, 6)
 R.FusedConsumer(t).run(100)
 paramfactory.safe_primes_u32(2, 200000)
+paramfactory.safe_primes_u32(2, 200000, literal_mr=True)
+st = R.init_vector(p, mv=1)
+R.take_floats(st, 4096 + 5)          # one thread per draw (K1p)
+st = R.init_vector(p, mv=64)
+R.take_raw(st, 64 * 200)             # K1p across 64 lanes
 src = bitsource.interstream_source(R.DEFAULT_MASTER_SEED, 0, 2, 8)
 stats.poker_test(src, 5000)
 stats.max_of_t_test(src, 8, 5000, 16)
