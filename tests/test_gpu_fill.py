@@ -554,3 +554,21 @@ def test_segmented_fill_stays_inside_its_buffers(p0, mv, blocks):
     assert bool((sc[:G] == 0xA5).all()) and bool((sc[G + nb:] == 0xA5).all())
     assert bool((f[:G] == -7.0).all()) and bool((f[G + n:] == -7.0).all())
     assert bool((f[G:G + n] >= 0).all()) and bool((f[G:G + n] < 1).all())
+
+
+@pytest.mark.parametrize("mv,blocks,flags", [(4096, 33, 0), (4095, 33, 0), (4096, 5, 8), (7, 9, 0)])
+def test_lane_fill_stays_inside_its_buffers(p0, mv, blocks, flags):
+    """Guard bands around rsa_fill's outputs (two-lane, one-lane and odd-Mv
+    paths)."""
+    from paper_1811_11629_b200 import _device
+    d = torch.device("cuda")
+    inst = rsacore.device_instance(p0, d)
+    m1, m2, s = vecgen._init_lanes(inst, 1, mv, 99, 1, d)
+    n, G = blocks * mv, 1024
+    r = torch.full((n + 2 * G,), 11, dtype=torch.int64, device=d)
+    f = torch.full((n + 2 * G,), -9.0, dtype=torch.float64, device=d)
+    _lib.call("rsa_fill", inst.data_ptr(), 1, mv, blocks, p0.e, _lib.RSA_FLAG_FAST | flags, m1.data_ptr(),
+              m2.data_ptr(), s.data_ptr(), r[G:].data_ptr(), f[G:].data_ptr(), n, _device.stream(d))
+    torch.cuda.synchronize()
+    assert bool((r[:G] == 11).all()) and bool((r[G + n:] == 11).all())
+    assert bool((f[:G] == -9.0).all()) and bool((f[G + n:] == -9.0).all())

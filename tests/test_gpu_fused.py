@@ -87,3 +87,22 @@ def test_many_instance_fill_config3(golden_meta):
     from conftest import sha
     for j, sid in enumerate(ids):
         assert sha(out[j].cpu().numpy().astype("<f8")) == golden_meta[f"c3_id{sid}_f64_sha256"], sid
+
+
+def test_fused_stays_inside_its_buffers():
+    """Guard bands around the per-instance statistics, histograms and lane
+    state (compute-sanitizer is closed on this pool); an instance count that
+    leaves idle lanes in the last CTA."""
+    from paper_1811_11629_b200 import _device, _lib
+    n, G = 130, 256
+    t = R.derive_params_table(SEED, 7, n)
+    fc = R.FusedConsumer(t)
+    d = t.device
+    stats = torch.full((n + 2 * G, 6), -3.0, dtype=torch.float64, device=d)
+    hist = torch.full((n + 2 * G, 64), -5, dtype=torch.int32, device=d)
+    _lib.call("rsa_fused_stats", t.inst.data_ptr(), n, 300, 9, fc.m1.data_ptr(), fc.m2.data_ptr(),
+              fc.s.data_ptr(), stats[G:].data_ptr(), hist[G:].data_ptr(), _device.stream(d))
+    torch.cuda.synchronize()
+    assert bool((stats[:G] == -3.0).all()) and bool((stats[G + n:] == -3.0).all())
+    assert bool((hist[:G] == -5).all()) and bool((hist[G + n:] == -5).all())
+    assert bool((hist[G:G + n].sum(dim=1) == 300).all())
