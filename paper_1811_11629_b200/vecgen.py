@@ -11,6 +11,7 @@ chunk computes.
 
 from __future__ import annotations
 
+from collections import OrderedDict
 from dataclasses import dataclass, field
 
 import torch
@@ -98,15 +99,64 @@ def _fill(state: VectorState, blocks: int, raw: torch.Tensor | None, f64: torch.
     nseg = int(L.rsa_fill_segments(state.mv, blocks))
     if nseg > 1 and flags & _lib.RSA_FLAG_FAST and (raw is not None or f64 is not None):
         nbytes = int(L.rsa_fill_segmented_scratch_bytes(state.mv, blocks))
-        scratch = torch.empty(nbytes, dtype=torch.uint8, device=d)
-        _lib.call("rsa_fill_segmented", inst.data_ptr(), 1, state.mv, blocks, p.e, flags,
-                  state.m1.data_ptr(), state.m2.data_ptr(), state.s.data_ptr(), out_r, out_f,
-                  blocks * state.mv, scratch.data_ptr(), nbytes, _device.stream(d))
+
+        def launch():
+            scratch = torch.empty(nbytes, dtype=torch.uint8, device=d)
+            _lib.call("rsa_fill_segmented", inst.data_ptr(), 1, state.mv, blocks, p.e, flags,
+                      state.m1.data_ptr(), state.m2.data_ptr(), state.s.data_ptr(), out_r, out_f,
+                      blocks * state.mv, scratch.data_ptr(), nbytes, _device.stream(d))
+            return scratch
+
+        key = (d.index, inst.data_ptr(), state.m1.data_ptr(), state.m2.data_ptr(), state.s.data_ptr(),
+               state.mv, blocks, p.e, flags, out_r, out_f)
+        _segmented_launch(key, launch, inst)
     else:
         _lib.call("rsa_fill", inst.data_ptr(), 1, state.mv, blocks, p.e, flags,
                   state.m1.data_ptr(), state.m2.data_ptr(), state.s.data_ptr(), out_r, out_f,
                   blocks * state.mv, _device.stream(d))
     state.draws += blocks * state.mv
+
+
+# Repeated segmented fills of one shape (the scalar stream / Mv = 64 takes of
+# a fixed size into a reused buffer) are launch-bound: the second identical
+# call captures the launches into a CUDA graph and later calls replay it
+# (kernel arguments are device pointers, so a replay reads the lane state as
+# it is then).  Bounded LRU; the entry keeps the instance record and the
+# graph's scratch alive.
+_GRAPHS: "OrderedDict[tuple, tuple]" = OrderedDict()
+_SEEN: "OrderedDict[tuple, None]" = OrderedDict()
+_GRAPH_MAX = 8
+
+
+def _segmented_launch(key: tuple, launch, keep: torch.Tensor) -> None:
+    hit = _GRAPHS.get(key)
+    if hit is not None:
+        _GRAPHS.move_to_end(key)
+        hit[0].replay()
+        return
+    if key not in _SEEN:
+        _SEEN[key] = None
+        if len(_SEEN) > 4 * _GRAPH_MAX:
+            _SEEN.popitem(last=False)
+        launch()
+        return
+    # capture on a side stream without torch.cuda.graph's synchronize /
+    # gc / empty_cache (only our own kernels are recorded)
+    cur = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
+    side.wait_stream(cur)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        g.capture_begin()
+        try:
+            scratch = launch()
+        finally:
+            g.capture_end()
+    cur.wait_stream(side)
+    _GRAPHS[key] = (g, keep, scratch)
+    if len(_GRAPHS) > _GRAPH_MAX:
+        _GRAPHS.popitem(last=False)
+    g.replay()
 
 
 def next_block_raw(state: VectorState) -> torch.Tensor:

@@ -572,3 +572,23 @@ def test_lane_fill_stays_inside_its_buffers(p0, mv, blocks, flags):
     torch.cuda.synchronize()
     assert bool((r[:G] == 11).all()) and bool((r[G + n:] == 11).all())
     assert bool((f[:G] == -9.0).all()) and bool((f[G + n:] == -9.0).all())
+
+
+@pytest.mark.parametrize("mv,n", [(1, 4096), (1, 1 << 16), (64, 64 * 600)])
+def test_repeated_takes_replay_graph_equal_stream(p0, mv, n):
+    """Identical segmented takes into a reused buffer are captured into a CUDA
+    graph on the second call and replayed after (vecgen._segmented_launch);
+    the concatenated outputs and the final state equal one long take."""
+    st = R.init_vector(p0, m0=5, mv=mv)
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    got = []
+    for _ in range(5):
+        R.take_floats(st, n, out=out)
+        got.append(u64np(out).copy())
+    assert any(k[5] == mv and k[6] == n // mv for k in vecgen._GRAPHS)
+    ref = R.init_vector(p0, m0=5, mv=mv)
+    want = u64np(R.take_floats(ref, 5 * n))
+    assert np.array_equal(np.concatenate(got), want)
+    for a, b in ((st.m1, ref.m1), (st.m2, ref.m2), (st.s, ref.s)):
+        assert torch.equal(a, b)
+    assert st.draws == ref.draws
