@@ -129,10 +129,15 @@ _GRAPH_MAX = 8
 
 
 def _segmented_launch(key: tuple, launch, keep: torch.Tensor) -> None:
+    d = keep.device
     hit = _GRAPHS.get(key)
     if hit is not None:
         _GRAPHS.move_to_end(key)
-        hit[0].replay()
+        if torch.cuda.current_device() == d.index:
+            hit[0].replay()
+        else:
+            with torch.cuda.device(d):
+                hit[0].replay()
         return
     if key not in _SEEN:
         _SEEN[key] = None
@@ -142,11 +147,11 @@ def _segmented_launch(key: tuple, launch, keep: torch.Tensor) -> None:
         return
     # capture on a side stream without torch.cuda.graph's synchronize /
     # gc / empty_cache (only our own kernels are recorded)
-    cur = torch.cuda.current_stream()
-    side = torch.cuda.Stream()
+    cur = torch.cuda.current_stream(d)
+    side = torch.cuda.Stream(device=d)
     side.wait_stream(cur)
     g = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(side):
+    with torch.cuda.device(d), torch.cuda.stream(side):
         g.capture_begin()
         try:
             scratch = launch()
@@ -156,7 +161,8 @@ def _segmented_launch(key: tuple, launch, keep: torch.Tensor) -> None:
     _GRAPHS[key] = (g, keep, scratch)
     if len(_GRAPHS) > _GRAPH_MAX:
         _GRAPHS.popitem(last=False)
-    g.replay()
+    with torch.cuda.device(d):
+        g.replay()
 
 
 def next_block_raw(state: VectorState) -> torch.Tensor:
