@@ -128,6 +128,12 @@ _SEEN: "OrderedDict[tuple, None]" = OrderedDict()
 _GRAPH_MAX = 8
 
 
+def clear_graph_cache() -> None:
+    """Drop the captured segmented-fill graphs (and the scratch they hold)."""
+    _GRAPHS.clear()
+    _SEEN.clear()
+
+
 def _segmented_launch(key: tuple, launch, keep: torch.Tensor) -> None:
     d = keep.device
     hit = _GRAPHS.get(key)

@@ -592,3 +592,5 @@ def test_repeated_takes_replay_graph_equal_stream(p0, mv, n):
     for a, b in ((st.m1, ref.m1), (st.m2, ref.m2), (st.s, ref.s)):
         assert torch.equal(a, b)
     assert st.draws == ref.draws
+    vecgen.clear_graph_cache()
+    assert not vecgen._GRAPHS
