@@ -128,6 +128,16 @@ int rsa_fill_segmented(const rsa_instance* inst, uint32_t n_inst, uint32_t mv, u
                        uint64_t* raw_out, double* f64_out, uint64_t inst_stride,
                        void* scratch, uint64_t scratch_bytes, void* stream);
 
+/* Scalar look-ahead (rsacore.next_raw / next_f64, rsacore.py:213-233): the
+ * next `count` draws (a multiple of 32, <= 32768) of the one-lane stream whose
+ * state is (m1, m2, s), with the state after every draw, so the host can
+ * serve single draws from a buffer and still expose the reference's state
+ * fields after each one.  `out` (device) receives count * 32 bytes:
+ * raw u64[count] | f64[count] | s u64[count] | m1 u32[count] | m2 u32[count].
+ * The caller's state is not modified.  Requires RSA_FLAG_FAST. */
+int rsa_scalar_lookahead(const rsa_instance* inst, uint64_t m1, uint64_t m2, uint64_t s,
+                         uint32_t e, uint32_t flags, uint32_t count, void* out, void* stream);
+
 /* floats_from_raw (vecgen.py:103-107): out[j] = min(fl(raw[j])/fl(n), 1-2^-53). */
 int rsa_floats_from_raw(const uint64_t* raw, uint64_t count, uint64_t n, double* out,
                         void* stream);

@@ -63,6 +63,7 @@ PROTOTYPES = {
     "rsa_floats_from_raw": (ctypes.c_int, [c_vp, c_u64, c_u64, c_vp, c_vp]),
     "rsa_skip_array": (ctypes.c_int, [c_vp, c_u64, c_u64, c_u64, c_vp, c_vp]),
     "rsa_fill_segments": (c_u64, [c_u64, c_u64]),
+    "rsa_scalar_lookahead": (ctypes.c_int, [c_vp, c_u64, c_u64, c_u64, c_u32, c_u32, c_u32, c_vp, c_vp]),
     "rsa_fill_segmented_scratch_bytes": (c_u64, [c_u64, c_u64]),
     "rsa_fill_segmented": (ctypes.c_int, [c_vp, c_u32, c_u32, c_u64, c_u32, c_u32, c_vp, c_vp, c_vp,
                                           c_vp, c_vp, c_u64, c_vp, c_u64, c_vp]),

@@ -353,6 +353,53 @@ k_pd_draws(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t blocks, 
     });
 }
 
+// ---- scalar look-ahead: the next `count` draws of one stream with every
+// intermediate state (rsacore.next_raw / next_f64 serve from it) ------------
+//
+// One warp; lane j owns draws [j*L, (j+1)*L): it jumps its skip to the
+// segment start, walks L skips (recording s), the warp scans the segments'
+// message increments, and each lane then walks its draws again writing the
+// raw value, the float and the state (m1, m2, s) after every draw.
+template <uint32_t E>
+__global__ void __launch_bounds__(32)
+k_scalar_lookahead(const rsa_instance* __restrict__ inst, uint64_t m1_0, uint64_t m2_0, uint64_t s_0,
+                   uint32_t L, uint64_t* __restrict__ raw, double* __restrict__ f64,
+                   uint64_t* __restrict__ ts, uint32_t* __restrict__ tm1, uint32_t* __restrict__ tm2) {
+    const FastInst P = load_fast(inst);
+    const uint32_t j = threadIdx.x;
+    const uint64_t k0 = (uint64_t)j * L;
+    uint64_t sk = seg_start(s_0, pow_q63(P.a, L), j);
+    uint32_t a1 = 0, a2 = 0;
+    for (uint32_t k = 0; k < L; ++k) {
+        sk = skip_q63(sk, P.a);
+        ts[k0 + k] = sk;
+        a1 = add_mod(a1, mont_redc(sk, P.p1, P.p1_inv), P.p1);
+        a2 = add_mod(a2, mont_redc(sk, P.p2, P.p2_inv), P.p2);
+    }
+    uint32_t e1 = a1, e2 = a2;
+    warp_scan2(e1, e2, P.p1, P.p2, j);
+    Lane Ln;
+    Ln.s = 0;
+    Ln.x1 = add_mod(mont_redc(m1_0, P.p1, P.p1_inv), sub_mod(e1, a1, P.p1), P.p1);
+    Ln.x2 = add_mod(mont_redc(m2_0, P.p2, P.p2_inv), sub_mod(e2, a2, P.p2), P.p2);
+    __syncwarp();
+    with_garner(P, [&](auto gf) {
+        constexpr bool GF = decltype(gf)::value;
+        for (uint32_t k = 0; k < L; ++k) {
+            const uint64_t v = ts[k0 + k];
+            Ln.x1 = add_mod(Ln.x1, mont_redc(v, P.p1, P.p1_inv), P.p1);
+            Ln.x2 = add_mod(Ln.x2, mont_redc(v, P.p2, P.p2_inv), P.p2);
+            uint32_t h, c2;
+            draw_tail<E, GF>(P, Ln, h, c2);
+            const uint64_t c = (uint64_t)h * P.p2 + c2;
+            raw[k0 + k] = c;
+            f64[k0 + k] = to_unit(c, P.n_float, P.n_recip, P.n_recip_lo);
+            tm1[k0 + k] = (uint32_t)lane_m1(P, Ln);
+            tm2[k0 + k] = (uint32_t)lane_m2(P, Ln);
+        }
+    });
+}
+
 }  // namespace rsa
 
 using namespace rsa;
@@ -492,4 +539,32 @@ extern "C" int rsa_fill_segmented(const rsa_instance* inst, uint32_t n_inst, uin
         default: launch_seg_fill<0>(grid, st, inst, mv, lanes, blocks, L, nseg_eff, m1, m2, s, st0, sums, raw_out, f64_out, inst_stride); break;
     }
     return launch_status("rsa_fill_segmented(fill)");
+}
+
+template <uint32_t E>
+static void launch_lookahead(cudaStream_t st, const rsa_instance* inst, uint64_t m1, uint64_t m2, uint64_t s,
+                             uint32_t L, char* out, uint32_t count) {
+    uint64_t* raw = reinterpret_cast<uint64_t*>(out);
+    double* f64 = reinterpret_cast<double*>(out + 8ull * count);
+    uint64_t* ts = reinterpret_cast<uint64_t*>(out + 16ull * count);
+    uint32_t* tm1 = reinterpret_cast<uint32_t*>(out + 24ull * count);
+    uint32_t* tm2 = reinterpret_cast<uint32_t*>(out + 28ull * count);
+    k_scalar_lookahead<E><<<1, 32, 0, st>>>(inst, m1, m2, s, L, raw, f64, ts, tm1, tm2);
+}
+
+extern "C" int rsa_scalar_lookahead(const rsa_instance* inst, uint64_t m1, uint64_t m2, uint64_t s,
+                                    uint32_t e, uint32_t flags, uint32_t count, void* out, void* stream) {
+    if (!inst || !out || e == 0 || count == 0 || count % 32 != 0 || count > 32u * 1024u) return RSA_EINVAL;
+    if (!(flags & RSA_FLAG_FAST)) return RSA_EPARAMS;
+    const uint32_t L = count / 32;
+    cudaStream_t st = as_stream(stream);
+    char* o = static_cast<char*>(out);
+    switch (e) {
+        case 3: launch_lookahead<3>(st, inst, m1, m2, s, L, o, count); break;
+        case 5: launch_lookahead<5>(st, inst, m1, m2, s, L, o, count); break;
+        case 9: launch_lookahead<9>(st, inst, m1, m2, s, L, o, count); break;
+        case 17: launch_lookahead<17>(st, inst, m1, m2, s, L, o, count); break;
+        default: launch_lookahead<0>(st, inst, m1, m2, s, L, o, count); break;
+    }
+    return launch_status("rsa_scalar_lookahead");
 }

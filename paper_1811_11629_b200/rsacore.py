@@ -269,14 +269,64 @@ def _scalar_run(state: GeneratorState, params: GeneratorParams, count: int, raw:
     return body.view(np.float64) if f64 else body
 
 
+# Single draws are served from a per-state look-ahead buffer that one GPU call
+# (rsa_scalar_lookahead) fills with the next LOOKAHEAD draws and the state
+# after each of them, so next_raw / next_f64 cost a buffer read instead of a
+# GPU round trip while the state's fields stay exactly the reference's after
+# every draw.  The buffer is tied to the state it was made from: any other
+# change to the state (take_raws, jump_periods, direct assignment) or a
+# different params object makes it refill.
+LOOKAHEAD = 512
+
+
+class _Lookahead:
+    __slots__ = ("params", "raw", "f64", "s", "m1", "m2", "pos", "expect")
+
+
+def _lookahead_draw(state: GeneratorState, params: GeneratorParams) -> tuple[_Lookahead, int] | None:
+    lk = state.__dict__.get("_lookahead")
+    if (lk is None or lk.pos >= LOOKAHEAD or (lk.params is not params and lk.params != params)
+            or lk.expect != (state.m1, state.m2, state.s, state.draws)):
+        if params.skip_mode != SKIP_LCG or not instance_flags(params) & _lib.RSA_FLAG_FAST:
+            return None
+        d = _device.device(None)
+        inst = device_instance(params, d)
+        buf = torch.empty(LOOKAHEAD * 32, dtype=torch.uint8, device=d)
+        _lib.call("rsa_scalar_lookahead", inst.data_ptr(), state.m1, state.m2, state.s, params.e,
+                  instance_flags(params), LOOKAHEAD, buf.data_ptr(), _device.stream(d))
+        host = buf.cpu().numpy()
+        n = LOOKAHEAD
+        lk = _Lookahead()
+        lk.params = params
+        lk.raw = host[:8 * n].view(np.uint64).tolist()
+        lk.f64 = host[8 * n:16 * n].view(np.float64).tolist()
+        lk.s = host[16 * n:24 * n].view(np.uint64).tolist()
+        lk.m1 = host[24 * n:28 * n].view(np.uint32).tolist()
+        lk.m2 = host[28 * n:32 * n].view(np.uint32).tolist()
+        lk.pos = 0
+        state.__dict__["_lookahead"] = lk
+    i = lk.pos
+    lk.pos = i + 1
+    state.m1, state.m2, state.s = lk.m1[i], lk.m2[i], lk.s[i]
+    state.draws += 1
+    lk.expect = (state.m1, state.m2, state.s, state.draws)
+    return lk, i
+
+
 def next_raw(state: GeneratorState, params: GeneratorParams) -> int:
     """Advance one step; the raw ciphertext c in [0, n) (rsacore.py:213-226)."""
-    return take_raws(state, params, 1)[0]
+    hit = _lookahead_draw(state, params)
+    if hit is None:
+        return take_raws(state, params, 1)[0]
+    return hit[0].raw[hit[1]]
 
 
 def next_f64(state: GeneratorState, params: GeneratorParams) -> float:
     """Next double in [0, 1) (rsacore.py:229-233)."""
-    return take_floats(state, params, 1)[0]
+    hit = _lookahead_draw(state, params)
+    if hit is None:
+        return take_floats(state, params, 1)[0]
+    return hit[0].f64[hit[1]]
 
 
 def take_raws(state: GeneratorState, params: GeneratorParams, count: int) -> list[int]:

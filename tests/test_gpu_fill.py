@@ -594,3 +594,46 @@ def test_repeated_takes_replay_graph_equal_stream(p0, mv, n):
     assert st.draws == ref.draws
     vecgen.clear_graph_cache()
     assert not vecgen._GRAPHS
+
+
+def test_scalar_lookahead_matches_reference_steps(p0):
+    """rsacore.next_raw / next_f64 served from the GPU look-ahead buffer: every
+    value and the state fields after every draw equal a Python-int walk of
+    the reference recurrence (rsacore.py:213-233), across refills, mixed with
+    take_raws, jump_periods and direct state edits (which invalidate the
+    buffer)."""
+    P = O.Params(p0.p1, p0.p2, p0.e, p0.skip.a)
+
+    def walk(m1, m2, s, k):
+        out = []
+        for _ in range(k):
+            s = P.a * s % P.q
+            m1, m2 = (m1 + s) % P.p1, (m2 + s) % P.p2
+            c2 = pow(m2, P.e, P.p2)
+            out.append(((pow(m1, P.e, P.p1) + P.p1 - c2 % P.p1) % P.p1 * P.p2inv % P.p1 * P.p2 + c2, m1, m2, s))
+        return out
+
+    st = rsacore.init(p0, m0=424242)
+    m1, m2, s = st.m1, st.m2, st.s
+    steps = walk(m1, m2, s, rsacore.LOOKAHEAD + 300)
+    for i, (c, a1, a2, sk) in enumerate(steps[:rsacore.LOOKAHEAD + 100]):
+        if i % 3 == 2:
+            r = rsacore.next_f64(st, p0)
+            assert r == min(float(c) / float(p0.n), O.MAX_BELOW_ONE), i
+        else:
+            assert rsacore.next_raw(st, p0) == c, i
+        assert (st.m1, st.m2, st.s, st.draws) == (a1, a2, sk, i + 1), i
+    # a bulk take in between, then single draws again (the buffer is stale)
+    k = rsacore.LOOKAHEAD + 100
+    assert rsacore.take_raws(st, p0, 50) == [x[0] for x in steps[k:k + 50]]
+    for c, a1, a2, sk in steps[k + 50:k + 80]:
+        assert rsacore.next_raw(st, p0) == c
+        assert (st.m1, st.m2, st.s) == (a1, a2, sk)
+    # direct edit of the state: the next draw follows the edited state
+    st.m1 = (st.m1 + 1) % p0.p1
+    want = walk(st.m1, st.m2, st.s, 2)
+    assert [rsacore.next_raw(st, p0) for _ in range(2)] == [w[0] for w in want]
+    # period jump (state fields change): still consistent
+    rsacore.jump_periods(st, p0, 3)
+    want = walk(st.m1, st.m2, st.s, 3)
+    assert [rsacore.next_raw(st, p0) for _ in range(3)] == [w[0] for w in want]
