@@ -283,7 +283,12 @@ class _Lookahead:
     __slots__ = ("params", "raw", "f64", "s", "m1", "m2", "pos", "expect")
 
 
-def _lookahead_draw(state: GeneratorState, params: GeneratorParams) -> tuple[_Lookahead, int] | None:
+def _lookahead_draw(state: GeneratorState, params: GeneratorParams, peek: bool = False):
+    """Serve the next draw from the state's look-ahead buffer (refilling it if
+    it does not continue this state); None when the instance has no fast
+    kernel.  peek=True only answers whether the buffer can serve."""
+    if peek:
+        return params.skip_mode == SKIP_LCG and bool(instance_flags(params) & _lib.RSA_FLAG_FAST)
     lk = state.__dict__.get("_lookahead")
     if (lk is None or lk.pos >= LOOKAHEAD or (lk.params is not params and lk.params != params)
             or lk.expect != (state.m1, state.m2, state.s, state.draws)):
@@ -329,13 +334,20 @@ def next_f64(state: GeneratorState, params: GeneratorParams) -> float:
     return hit[0].f64[hit[1]]
 
 
+_SMALL_TAKE = 64  # takes up to this size are served from the look-ahead buffer
+
+
 def take_raws(state: GeneratorState, params: GeneratorParams, count: int) -> list[int]:
     """count sequential raw draws (rsacore.py:236-258)."""
+    if 0 < count <= _SMALL_TAKE and _lookahead_draw(state, params, peek=True):
+        return [next_raw(state, params) for _ in range(count)]
     return _scalar_run(state, params, count, True, False).tolist()
 
 
 def take_floats(state: GeneratorState, params: GeneratorParams, count: int) -> list[float]:
     """count sequential next_f64 draws (rsacore.py:261-264)."""
+    if 0 < count <= _SMALL_TAKE and _lookahead_draw(state, params, peek=True):
+        return [next_f64(state, params) for _ in range(count)]
     return _scalar_run(state, params, count, False, True).tolist()
 
 
