@@ -18,10 +18,20 @@ namespace rsa {
 constexpr int FUSED_BLOCK = 128;
 constexpr uint64_t FLUSH_MASK = (1u << 15) - 1;
 
-RSA_DEV void flush_hist(uint16_t* h, uint32_t* gh, bool active) {
+#ifndef RSA_FUSED_HIST32
+#define RSA_FUSED_HIST32 0
+#endif
+#if RSA_FUSED_HIST32
+typedef uint32_t hist_t;  // A/B: u32 counters bumped with shared-memory atomics
+#define RSA_HIST_BUMP(p) atomicAdd((p), 1u)
+#else
+typedef uint16_t hist_t;
+#define RSA_HIST_BUMP(p) (*(p) += 1)
+#endif
+RSA_DEV void flush_hist(hist_t* h, uint32_t* gh, bool active) {
 #pragma unroll 8
     for (int b = 0; b < 64; ++b) {
-        uint16_t v = h[b * FUSED_BLOCK + threadIdx.x];
+        hist_t v = h[b * FUSED_BLOCK + threadIdx.x];
         if (v) {
             if (active) gh[b] += v;
             h[b * FUSED_BLOCK + threadIdx.x] = 0;
@@ -37,7 +47,7 @@ __global__ void __launch_bounds__(FUSED_BLOCK, RSA_FUSED_MINB)
 k_fused(const rsa_instance* __restrict__ inst, uint32_t n_inst, uint64_t draws,
         uint64_t* __restrict__ m1, uint64_t* __restrict__ m2, uint64_t* __restrict__ s,
         rsa_fused_stat* __restrict__ stats, uint32_t* __restrict__ hist) {
-    __shared__ uint16_t h[64 * FUSED_BLOCK];
+    __shared__ hist_t h[64 * FUSED_BLOCK];
     const uint32_t tid = threadIdx.x;
     const uint32_t i = blockIdx.x * FUSED_BLOCK + tid;
     const bool active = i < n_inst;
@@ -49,7 +59,7 @@ k_fused(const rsa_instance* __restrict__ inst, uint32_t n_inst, uint64_t draws,
     for (int b = 0; b < 64; ++b) h[b * FUSED_BLOCK + tid] = 0;
     if (active)
         for (int b = 0; b < 64; ++b) gh[b] = 0;
-    uint16_t* hb = h + tid;
+    hist_t* hb = h + tid;
 
     double s1 = 0.0, s2 = 0.0, lag = 0.0, xy = 0.0, prev = 0.0, first = 0.0;
     // chunks of <= 2^15 draws: the u16 counters cannot wrap inside a chunk, and
@@ -69,7 +79,7 @@ k_fused(const rsa_instance* __restrict__ inst, uint32_t n_inst, uint64_t draws,
                 s2 = __dmul_rn(r, r);
                 double o = __shfl_xor_sync(0xffffffffu, r, 1);
                 xy = __dmul_rn(r, o);
-                hb[(uint32_t)__double2loint(__fma_rz(r, 64.0, 0x1p52)) * FUSED_BLOCK] += 1;
+                RSA_HIST_BUMP(&hb[(uint32_t)__double2loint(__fma_rz(r, 64.0, 0x1p52)) * FUSED_BLOCK]);
                 prev = r;
                 kk = 1;
             }
@@ -84,7 +94,7 @@ k_fused(const rsa_instance* __restrict__ inst, uint32_t n_inst, uint64_t draws,
                 xy = __fma_rn(r, o, xy);
                 // floor(64 r) exactly: 2^52 + 64r rounded toward zero keeps the integer part
                 uint32_t b = (uint32_t)__double2loint(__fma_rz(r, 64.0, 0x1p52));
-                hb[b * FUSED_BLOCK] += 1;
+                RSA_HIST_BUMP(&hb[b * FUSED_BLOCK]);
             }
             done += len;
             flush_hist(h, gh, active);
