@@ -1,62 +1,55 @@
 """Benchmark harness (driver contract: one JSON line from rank 0).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2|3|4|5] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..6] [--impl ours|reference]
 
-Default workload = BASELINE.json configs[1] ("single instance bulk fill"):
-per rank one generator instance (stream id = rank, DEFAULT_MASTER_SEED), Mv =
-2^22 lanes, seeded uniform m0 in [0, n), and for each exponent e in
-{3, 5, 17, 65537} a fill of 2^30 float64 outputs (256 blocks) into HBM.  One
-step = those four fills.  Ranks are independent instances (weak scaling, no
-data-path collective).  Outputs are 8 GiB per fill (> 126 MB L2), so
-every timed fill streams to HBM without an explicit flush.
+`--gpus N` with N > 1 outside torchrun re-launches this script under
+`torch.distributed.run --nproc-per-node N` (127.0.0.1); under torchrun the
+world size must equal N.  One process per GPU, NCCL.
 
-`value`    Gnumbers/s over all ranks, device-timed (CUDA events, max over ranks).
-`e2e`      same metric through the public API with the lane state resumed
-           from pinned host memory and every output copied to pinned host
-           memory (vecgen.take_floats(out=host) pipelines the D2H behind the
-           next chunk's compute).
-`roofline` the dominant kernel (largest share of the step) against the
-           measured Montgomery-triple IMAD peak, plus its
-           HBM write fraction.
-`cpu_baseline` the numpy port of the reference's lockstep path (oracle/) on
-           a bounded sample, all host cores.
+Default run: BASELINE.json configs[1] ("single instance bulk fill") is the
+headline `value`; the other configurations are measured in the same run and
+reported under `configs` (bench_configs.py holds the workloads):
+
+  value    config 2: per rank one generator instance (stream id = rank), Mv =
+           2^22, seeded m0; for each e in {3, 5, 17, 65537} a fill of 2^30
+           float64 (256 blocks) into HBM.  One step = the four fills.  Weak
+           scaling (independent instances, no data-path collective).  Outputs
+           are 8 GiB per fill (> 126 MB L2): no flush needed.
+  configs  "1" (stream 0, 2^20 draws at Mv 1/64/65536), "3" (65,536 instances,
+           strong scaling), "4" (2^20 instances fused + all-reduce, strong),
+           "5" (safe-prime census + 2^20 tuples): each with its own value,
+           device-timed K-step blocks, clocks, roofline and (N = 1) cpu_baseline.
+
+`e2e`      config 2 through the public API with the lane state resumed from
+           pinned host memory and every output copied to pinned host memory.
+`roofline` the dominant kernel of config 2 against the measured
+           Montgomery-triple IMAD peak, plus its HBM fraction.
+`cpu_baseline` the reference's algorithm (oracle/ port) on bounded samples,
+           all host cores, rank 0 at N = 1 only.
 `--impl reference` times that same CPU port as the reference arm.
 """
 
 from __future__ import annotations
 
 import argparse
-import dataclasses
 import json
-import math
-import multiprocessing as mp
 import os
+import socket
 import statistics
 import subprocess
 import sys
 import threading
 import time
 
-import numpy as np
-
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-EXPONENTS = (3, 5, 17, 65537)
-MV = 1 << 22
-BLOCKS = 256
-M0_RNG_SEED = 181111629
+import bench_configs as C  # noqa: E402
+from bench_configs import EXPONENTS, cpu_port_rate, seeded_m0, w_imad  # noqa: E402,F401
+
 METRIC = "RSA-PRNG Gnumbers/s at 1/2/4/8 B200; % of IMAD/HBM roofline; vs CPU"
-
-
-def w_imad(e: int) -> int:
-    """Algorithmic IMAD-class ops per draw, W(e) = 6 M(e) + 13."""
-    m = e.bit_length() - 1 + bin(e).count("1") - 1
-    return 6 * m + 13
-
-
-def seeded_m0(n: int) -> int:
-    return int(np.random.default_rng(M0_RNG_SEED).integers(0, n, dtype=np.uint64))
+SUB_CONFIGS = (1, 3, 4, 5)
+MIN_REGION_S = 0.5  # short steps are timed in repeated K-step blocks until the sampler saw this much
 
 
 def peaks() -> dict:
@@ -79,6 +72,7 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines: list[str] = []
+        self._first = threading.Event()
 
     def __enter__(self):
         try:
@@ -88,6 +82,7 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            self._first.wait(timeout=5.0)  # sampling has started before the timed region
         except OSError:
             self.proc = None
         return self
@@ -95,6 +90,8 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+            self._first.set()
+        self._first.set()
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -117,49 +114,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU port (oracle) — cpu_baseline and the reference arm
-
-def _cpu_worker(args):
-    e_list, blocks, mv, seed_idx = args
-    from oracle import rsa_oracle as O
-    import json as _json
-    with open(os.path.join(ROOT, "tests", "golden", "regression.json")) as fh:
-        P0 = O.from_fields(_json.load(fh)["params"])
-    st = O.init(P0, m0=seeded_m0(P0.n), mv=mv)
-    out = {}
-    for e in e_list:
-        P = dataclasses.replace(P0, e=e)
-        m1, m2, s = st.m1.copy(), st.m2.copy(), st.s.copy()
-        O.block_raw(m1, m2, s, P)  # warm-up
-        t0 = time.perf_counter()
-        for _ in range(blocks):
-            raw, m1, m2, s = O.block_raw(m1, m2, s, P)
-            O.floats_from_raw(raw, P)
-        out[e] = (blocks * mv, time.perf_counter() - t0)
-    return out
-
-
-def cpu_port_rate(procs: int | None = None, blocks: int = 4, mv: int = 65536) -> dict:
-    """Aggregate numbers/s of the numpy port of vecgen's lockstep path
-    (Mv=65536, the reference CLI bench default, cli.py:26) over all host cores,
-    with the step's exponent mix weighted equally per draw."""
-    procs = procs or os.cpu_count() or 1
-    with mp.get_context("fork").Pool(procs) as pool:
-        res = pool.map(_cpu_worker, [(EXPONENTS, blocks, mv, i) for i in range(procs)])
-    per_e = {}
-    for e in EXPONENTS:
-        draws = sum(r[e][0] for r in res)
-        wall = max(r[e][1] for r in res)
-        per_e[e] = draws / wall
-    # one step draws equally at each e: time per draw = mean of 1/rate
-    rate = len(EXPONENTS) / sum(1.0 / per_e[e] for e in EXPONENTS)
-    draws = sum(r[e][0] for r in res for e in EXPONENTS)
-    return {"value": rate / 1e9, "unit": "Gnumbers/s", "cores": procs, "kind": "port",
-            "per_e": {str(e): per_e[e] / 1e9 for e in EXPONENTS},
-            "sample": f"numpy port of vecgen lockstep (oracle/rsa_oracle.py), Mv={mv}, {blocks} "
-                      f"blocks per e in {list(EXPONENTS)} per process, {procs} processes "
-                      f"({draws} draws), stream 0 seeded m0; {os.cpu_count()} host cores"}
-
+# reference arm: the reference's algorithm (oracle/ port) on the host cores
 
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
@@ -189,20 +144,38 @@ def run_reference_arm(args):
 
 
 # ---------------------------------------------------------------------------
-# GPU arm
+# process launch and distributed plumbing
 
-def dist_setup(args):
+def _free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(args, argv) -> int:
+    """`--gpus N` outside torchrun: start N ranks (one per GPU) under
+    torch.distributed.run on this node and return its exit status."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
+
+
+def dist_setup(args, cpu: bool = False):
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch N ranks with "
+                         f"torchrun --nproc-per-node N, or run without torchrun and let bench.py spawn them)")
     # RSARAND_BENCH_BACKEND=gloo exercises the multi-rank path on fewer GPUs
     # than ranks (harness check only; ranks never wait on one another in a kernel)
-    backend = os.environ.get("RSARAND_BENCH_BACKEND", "nccl")
-    if backend == "gloo":
-        local = local % torch.cuda.device_count()
-    torch.cuda.set_device(local)
+    backend = "gloo" if cpu else os.environ.get("RSARAND_BENCH_BACKEND", "nccl")
+    if not cpu:
+        if backend == "gloo":
+            local = local % torch.cuda.device_count()
+        torch.cuda.set_device(local)
     if world > 1:
         if backend == "gloo":
             dist.init_process_group("gloo")
@@ -230,110 +203,141 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
+def launch_check(args) -> int:
+    """CPU-only harness check of the launcher: every rank joins a gloo group
+    and rank 0 prints the world it saw (tests/test_multirank.py)."""
+    import torch.distributed as dist
+    world, rank, _ = dist_setup(args, cpu=True)
+    ranks = [rank]
+    if world > 1:
+        got = [None] * world
+        dist.all_gather_object(got, {"rank": rank, "pid": os.getpid()})
+        ranks = [g["rank"] for g in got]
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": world, "ranks": ranks}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def probe_imad_peak(dev) -> dict:
     """Measured Montgomery-triple IMAD-class rate (ops/s) on this GPU."""
+    import ctypes
     import torch
     from paper_1811_11629_b200 import _lib
     sink = torch.zeros(1, dtype=torch.int32, device=dev)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     grid, iters = sms * 8, 8192
-    ops = __import__("ctypes").c_double(0)
+    ops = ctypes.c_double(0)
     st = torch.cuda.current_stream(dev)
     best = 0.0
     for _ in range(4):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
-        _lib.call("rsa_probe_imad", grid, iters, sink.data_ptr(), __import__("ctypes").byref(ops), st.cuda_stream)
+        _lib.call("rsa_probe_imad", grid, iters, sink.data_ptr(), ctypes.byref(ops), st.cuda_stream)
         b.record(st)
         b.synchronize()
         best = max(best, ops.value / (a.elapsed_time(b) * 1e-3))
     return {"ops_per_s": best, "sms": sms}
 
 
-def run_config2(args, world, rank, local):
+def count_launches(fn) -> int | None:
+    """Kernels of this repo's library launched by one call of `fn` (an extra,
+    untimed step), counted from the CUDA activity trace (CUPTI via
+    torch.profiler).  None when the profiler is unavailable."""
     import torch
-    import paper_1811_11629_b200 as R
-    from paper_1811_11629_b200 import vecgen
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        n = 0
+        for ev in prof.events():
+            name = ev.name or ""
+            if ev.device_type == torch.autograd.DeviceType.CUDA and "rsa::" in name:
+                n += 1
+        return n
+    except Exception:  # pragma: no cover - profiler missing on the box
+        return None
 
-    dev = torch.device("cuda", local)
-    base = R.derive_stream_params(R.StreamKey(R.DEFAULT_MASTER_SEED, rank))
-    m0 = seeded_m0(base.n)
-    params = {e: dataclasses.replace(base, e=e) for e in EXPONENTS}  # e=65537 bypasses validation
-    st0 = R.init_vector(base, m0=m0, mv=MV, device=dev)
-    states = {e: vecgen.VectorState(params=params[e], mv=MV, m1=st0.m1.clone(), m2=st0.m2.clone(),
-                                    s=st0.s.clone()) for e in EXPONENTS}
-    count = MV * BLOCKS
-    out = torch.empty(count, dtype=torch.float64, device=dev)
-    stream = torch.cuda.current_stream(dev)
 
-    def step(events=None):
-        for e in EXPONENTS:
-            if events is not None:
-                events[e][0].record(stream)
-            if args.one_lane:
-                _fill_flags(states[e], count, out, 8)
-            else:
-                R.take_floats(states[e], count, out=out)
-            if events is not None:
-                events[e][1].record(stream)
+# ---------------------------------------------------------------------------
+# timing
 
-    peak = probe_imad_peak(dev)
+def time_workload(w, args, world, local, events_keys=(), min_region_s=0.0):
+    """W untimed warm-up steps, then K-step blocks bracketed by barrier +
+    synchronize, CUDA events on the launch stream, max over ranks.  Short
+    steps repeat the K-step block until the clock sampler has watched at
+    least `min_region_s` of timed work; the block time reported is the median.
+    Returns (seconds per K-step block, clock summary, per-key mean seconds of
+    the first block's sub-events)."""
+    import torch
+    stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
-        step()
-    ev = {e: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(args.steps)] for e in EXPONENTS}
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w.step()
+    ev = None
+    if events_keys:
+        ev = {k: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(args.steps)] for k in events_keys}
+    blocks = []
     barrier_sync(world)
     with ClockSampler(local) as clk:
-        t0.record(stream)
-        for k in range(args.steps):
-            step({e: ev[e][k] for e in EXPONENTS})
-        t1.record(stream)
-        barrier_sync(world)
-    elapsed = t0.elapsed_time(t1) * 1e-3
-    elapsed_max = max_over_ranks(elapsed, world)
-    per_e = {e: statistics.mean(a.elapsed_time(b) * 1e-3 for a, b in ev[e]) for e in EXPONENTS}
-    clk_summary = clk.summary()
-    total_numbers = world * args.steps * len(EXPONENTS) * count
-    value = total_numbers / elapsed_max / 1e9
+        while True:
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier_sync(world)
+            t0.record(stream)
+            for k in range(args.steps):
+                if ev is not None and not blocks:
+                    w.step({key: ev[key][k] for key in events_keys})
+                else:
+                    w.step()
+            t1.record(stream)
+            barrier_sync(world)
+            blocks.append(max_over_ranks(t0.elapsed_time(t1) * 1e-3, world))
+            if sum(blocks) >= min_region_s or len(blocks) >= 200:
+                break
+    per_key = {}
+    if ev is not None:
+        per_key = {k: statistics.mean(a.elapsed_time(b) * 1e-3 for a, b in ev[k]) for k in events_keys}
+    return statistics.median(blocks), clk.summary(), per_key, len(blocks)
 
-    # dominant kernel: largest share of the step
-    dom = max(EXPONENTS, key=lambda e: per_e[e])
-    imad_ach = w_imad(dom) * count / per_e[dom]
-    pk = peaks()
-    hbm_peak = pk.get("hbm_gbs")
-    traffic = load_traffic(f"fill_e{dom}")
-    lpt = 1 if args.one_lane else 2
-    roofline = {"bound": "imad", "kernel": f"k_fill_fast<{dom}, {lpt}, 0, 1> (e={dom})",
-                "achieved": imad_ach / 1e12, "peak": peak["ops_per_s"] / 1e12, "unit": "Tops/s",
-                "frac": imad_ach / peak["ops_per_s"], "traffic": traffic,
-                "algorithmic_ops_per_draw": w_imad(dom), "draws_per_launch": count,
-                "launch_ms": per_e[dom] * 1e3,
-                "peak_source": "measured in-run: rsa_probe_imad Montgomery-triple stream (IMAD-class ops/s)",
-                "hbm": {"achieved_gbs": 8 * count / per_e[dom] / 1e9, "peak_gbs": hbm_peak,
-                        "frac": (8 * count / per_e[dom] / 1e9 / hbm_peak) if hbm_peak else None,
-                        "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)"},
-                "heavy_pipe": heavy_pipe(f"fill_e{dom}", count, per_e[dom], peak, clk_summary),
-                "per_exponent": {str(e): {"ms": per_e[e] * 1e3, "gnumbers_s": count / per_e[e] / 1e9,
-                                          "imad_frac": w_imad(e) * count / per_e[e] / peak["ops_per_s"],
-                                          "hbm_frac": (8 * count / per_e[e] / 1e9 / hbm_peak) if hbm_peak else None}
-                                 for e in EXPONENTS}}
 
-    # e2e through the public API: state resumed from pinned host, outputs to pinned host
+# ---------------------------------------------------------------------------
+# configurations
+
+def run_config2(args, world, rank, local, dev, peak):
+    import torch
+    w = C.Config2(dev, world, rank)
+    R = w.R
+    count = w.count
+    el, clk, per_e, nblocks = time_workload(w, args, world, local, events_keys=EXPONENTS)
+    value = w.numbers_per_step * args.steps / el / 1e9
+    dom = max(EXPONENTS, key=lambda e: per_e[e])  # dominant kernel: largest share of the step
+    roofline = C.imad_roofline(dom, count, per_e[dom], peak, f"k_fill_fast<{dom}, 2, 0, 1> (e={dom})",
+                               f"fill_e{dom}", f"fill_e{dom}", clk)
+    roofline["per_exponent"] = {
+        str(e): {"ms": per_e[e] * 1e3, "gnumbers_s": count / per_e[e] / 1e9,
+                 "imad_frac": w_imad(e) * count / per_e[e] / peak["ops_per_s"],
+                 "hbm_frac": roofline["hbm"]["frac"] * per_e[dom] / per_e[e] if roofline["hbm"]["frac"] else None}
+        for e in EXPONENTS}
+    launches = count_launches(w.step)
+
     e2e = None
     if not args.no_e2e:
+        # the public API end to end: lane state resumed from pinned host memory,
+        # every output copied to pinned host memory (take_floats(out=host))
         host_out = torch.empty(count, dtype=torch.float64, pin_memory=True)
-        host_state = {e: [t.cpu().pin_memory() for t in (states[e].m1, states[e].m2, states[e].s)]
+        host_state = {e: [t.cpu().pin_memory() for t in (w.states[e].m1, w.states[e].m2, w.states[e].s)]
                       for e in EXPONENTS}
         e2e_steps = max(1, min(args.steps, 2))
-        # untimed warm-up: one pass over the pinned buffer (first DMA touch of 8 GiB)
-        R.take_floats(states[EXPONENTS[0]], count, out=host_out)
+        R.take_floats(w.states[EXPONENTS[0]], count, out=host_out)  # first DMA touch of 8 GiB, untimed
         barrier_sync(world)
         t = time.perf_counter()
         for _ in range(e2e_steps):
             for e in EXPONENTS:
-                hs = host_state[e]
-                st = states[e]
+                hs, st = host_state[e], w.states[e]
                 st.m1.copy_(hs[0], non_blocking=True)
                 st.m2.copy_(hs[1], non_blocking=True)
                 st.s.copy_(hs[2], non_blocking=True)
@@ -341,95 +345,155 @@ def run_config2(args, world, rank, local):
         barrier_sync(world)
         e2e_t = max_over_ranks(time.perf_counter() - t, world)
         e2e = {"value": world * e2e_steps * len(EXPONENTS) * count / e2e_t / 1e9, "unit": "Gnumbers/s",
-               "h2d_bytes_per_step": len(EXPONENTS) * 3 * 8 * MV,
+               "h2d_bytes_per_step": len(EXPONENTS) * 3 * 8 * w.MV,
                "d2h_bytes_per_step": len(EXPONENTS) * 8 * count,
                "steps": e2e_steps, "path": "vecgen.take_floats(state, 2^30, out=pinned host)"}
+        del host_out, host_state
 
     line = {"metric": METRIC, "value": value, "unit": "Gnumbers/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_max / args.steps * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u32 Montgomery / u64 skip + f64 map",
             "data": "synthetic: derived stream params (DEFAULT_MASTER_SEED, stream id = rank), "
                     "seeded uniform m0 in [0, n)",
             "config": {"workload": "config2 bulk fill: 2^30 f64 per exponent e in {3,5,17,65537}, "
                                    "Mv=2^22, 256 blocks, one instance per GPU",
-                       "global_numbers_per_step": total_numbers // args.steps,
-                       "mv": MV, "blocks": BLOCKS, "exponents": list(EXPONENTS), "m0": m0,
+                       "global_numbers_per_step": w.numbers_per_step,
+                       "mv": w.MV, "blocks": w.BLOCKS, "exponents": list(EXPONENTS), "m0": w.m0,
                        "l2": "outputs 8 GiB per fill (> L2), no flush needed",
                        "parallelism": f"independent instances x{world}"},
-            "roofline": roofline, "clocks": clk_summary, "gpu_launches": args.steps * len(EXPONENTS),
+            "roofline": roofline, "clocks": clk,
+            "gpu_launches": launches * args.steps if launches is not None else args.steps * len(EXPONENTS),
+            "gpu_launches_source": "CUPTI kernel trace of one extra step x K" if launches is not None
+            else "static count (profiler unavailable)",
             "e2e": e2e, "imad_peak_tops": peak["ops_per_s"] / 1e12,
             "published_context": ("BASELINE.md: the paper's C/OpenMP generator on a 24-core Xeon E5-2680 v3 "
                                   "reached 1.25e8-1.72e8 numbers/s at e <= 17 (PAPER.md:420-421); a different "
                                   "implementation, hardware and exponent mix, so vs_baseline stays null")}
-    return line
+    del w
+    return line, None
 
 
-def _fill_flags(state, count, out, extra):
-    """A/B only: rsa_fill with extra RSA_FLAG_* hints for whole blocks."""
-    from paper_1811_11629_b200 import _device, _lib, rsacore
-    p = state.params
-    inst = rsacore.device_instance(p, state.device)
-    _lib.call("rsa_fill", inst.data_ptr(), 1, state.mv, count // state.mv, p.e,
-              _lib.RSA_FLAG_FAST | extra, state.m1.data_ptr(), state.m2.data_ptr(),
-              state.s.data_ptr(), None, out.data_ptr(), count, _device.stream(state.device))
+def _sub_line(args, world, value, unit, el, clk, nblocks, config, scaling, launches, static_launches):
+    return {"value": value, "unit": unit, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": el / args.steps * 1e3, "timed_blocks": nblocks, "scaling": scaling,
+            "higher_is_better": True, "config": config, "clocks": clk,
+            "gpu_launches": launches * args.steps if launches is not None else static_launches * args.steps}
 
 
-def load_slots(key: str):
-    try:
-        with open(os.path.join(ROOT, "profiles", "slots.json")) as fh:
-            return json.load(fh).get(key)
-    except (OSError, ValueError):
-        return None
+def run_config1(args, world, rank, local, dev, peak):
+    w = C.Config1(dev, world, rank)
+    el, clk, per_mv, nblocks = time_workload(w, args, world, local, events_keys=w.MVS,
+                                             min_region_s=MIN_REGION_S)
+    line = _sub_line(args, world, w.numbers_per_step * args.steps / el / 1e9, "Gnumbers/s", el, clk, nblocks,
+                     {"workload": "config1: stream 0, e=9, 2^20 f64 per take_floats at Mv=1, 64, 65536 "
+                                  "(< 2^17 lanes: split across threads by K1p/K1s, graph-replayed)"},
+                     "weak", count_launches(w.step), 6)
+    line["per_mv"] = {str(mv): {"ms_per_2e20": per_mv[mv] * 1e3, "gnumbers_s": w.COUNT / per_mv[mv] / 1e9}
+                      for mv in w.MVS}
+    dom = max(w.MVS, key=lambda mv: per_mv[mv])
+    rf = C.imad_roofline(9, w.COUNT, per_mv[dom], peak, f"take_floats(2^20) at Mv={dom}", None, None, clk)
+    rf["bound"] = "latency"
+    rf["note"] = "2^20 draws per call: a few us of kernel work per launch; launch/latency-bound"
+    line["roofline"] = rf
+    line["reference_context"] = ("reference scalar rsacore.take_raws 2.35 us/draw (4.26e5/s) and "
+                                 "vecgen bench_throughput 1.18e7/s at Mv=65536, one core (SURVEY §6)")
+    return line, None
 
 
-def heavy_pipe(key: str, draws: int, seconds: float, peak: dict, clk: dict) -> dict | None:
-    """The datapath that actually bounds the kernel: IMAD.WIDE/IMAD.HI (2
-    slots), IMAD and FP64 ops (1 slot) share 64 slots/clk/SM on B200
-    (profiles/r01_probe_hybrid.txt).  Slots per draw are counted from the SASS
-    (tools/slots_json.py -> profiles/slots.json); the measured peak is the
-    in-run Montgomery-triple probe (3 instructions = 5 slots)."""
-    spd = load_slots(key)
-    if not spd:
-        return None
-    ach = spd * draws / seconds
-    meas = peak["ops_per_s"] * 5.0 / 3.0
-    out = {"slots_per_draw": spd, "achieved_tslots": ach / 1e12, "peak_tslots_measured": meas / 1e12,
-           "frac_of_measured": ach / meas}
-    if clk.get("sm_mhz"):
-        nominal = 64.0 * peak["sms"] * clk["sm_mhz"] * 1e6
-        out["peak_tslots_nominal_at_clock"] = nominal / 1e12
-        out["frac_of_nominal"] = ach / nominal
-    return out
+def run_config3(args, world, rank, local, dev, peak):
+    w = C.Config3(dev, world, rank)
+    el, clk, _, nblocks = time_workload(w, args, world, local)
+    per = el / args.steps
+    line = _sub_line(args, world, w.numbers_per_step * args.steps / el / 1e9, "Gnumbers/s", el, clk, nblocks,
+                     {"workload": "config3: 65536 instances (ids 0..65535), e=9, Mv=64, 1024 blocks, "
+                                  "2^16 f64 each, instance-major, sharded by contiguous id range",
+                      "shard": [w.first, w.n], "l2": "32 GiB output per step (> L2)"},
+                     "strong", count_launches(w.step), 1)
+    line["roofline"] = C.imad_roofline(9, w.local_numbers, per, peak, "k_fill_fast<9, 2, 0, 1>", "fill_c3",
+                                       "fill_e9", clk)
+    table = w.table
+    del w
+    return line, table
 
 
-def load_traffic(key: str):
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            return json.load(fh).get(key)
-    except (OSError, ValueError):
-        return None
+def run_config4(args, world, rank, local, dev, peak):
+    w = C.Config4(dev, world, rank)
+    el, clk, _, nblocks = time_workload(w, args, world, local)
+    per = el / args.steps
+    line = _sub_line(args, world, w.numbers_per_step * args.steps / el / 1e9, "Gnumbers/s", el, clk, nblocks,
+                     {"workload": "config4 fused consumer: 2^20 instances x 2^16 draws, Mv=1, e=9; "
+                                  "per-instance mean/var/lag-1/64-bin hist + pooled pair correlation; "
+                                  "NCCL all-reduce of pooled stats at N>1", "shard": [w.first, w.n],
+                      "l2": "no stream in HBM"},
+                     "strong", count_launches(w.step), 3)
+    line["roofline"] = C.imad_roofline(9, w.local_numbers, per, peak, "k_fused<9>", "fused", "fused_e9", clk,
+                                       hbm_bytes_per_draw=0)
+    line["pooled_correlation"] = w.result.pooled_correlation(w.TOTAL // 2)
+    table = w.table
+    del w
+    return line, table
+
+
+def run_config5(args, world, rank, local, dev, peak):
+    w = C.Config5(dev, world, rank)
+
+    class Timed:  # the step plus its phase bookkeeping
+        def step(self_inner):
+            w.step()
+            w.collect()
+
+    el, clk, _, nblocks = time_workload(Timed(), args, world, local, min_region_s=MIN_REGION_S)
+    line = _sub_line(args, world, w.numbers_per_step * args.steps / el / 1e9, "Gcandidates/s", el, clk, nblocks,
+                     {"workload": "config5 setup: safe-prime scan (sieve to 8191, base-2 SPRP, spsp(2) table) "
+                                  "of all 2^30 odd candidates in [2^31,2^32) + 2^20 instance tuples "
+                                  "(ids 0..2^20-1)",
+                      "unit_note": "value = odd candidates per second (scan + tuples in the step; at N>1 the "
+                                   "scan phase includes the all-gather of the per-rank counts and lists)"},
+                     "strong", count_launches(w.step), 8)
+    scan_ms = statistics.median(w.phase["scan"])
+    setup_ms = statistics.median(w.phase["setup"])
+    line["phases"] = {"scan_ms": scan_ms, "scan_gcandidates_s": (w.hi - w.lo) // 2 / (scan_ms * 1e-3) / 1e9,
+                      "safe_primes_found": w.count, "setup_ms": setup_ms,
+                      "tuples_per_s": w.n / (setup_ms * 1e-3)}
+    if world == 1:
+        lm = C.literal_mr_scan(args.steps, w.lo, w.hi, dev, w.count, peak)
+        line["literal_mr"] = lm
+        line["roofline"] = dict(lm["roofline"], note="literal MR(2,7,61) census kernels; the production scan "
+                                                     "is sieve/issue-bound (profiles/r01_ncu_scan.md)")
+    return line, None
+
+
+RUNNERS = {1: run_config1, 2: run_config2, 3: run_config3, 4: run_config4, 5: run_config5}
 
 
 def run_gpu(args):
+    import torch
     world, rank, local = dist_setup(args)
-    if args.config == 2:
-        line = run_config2(args, world, rank, local)
+    dev = torch.device("cuda", local)
+    peak = probe_imad_peak(dev)
+    if args.config == 6:
+        from bench_configs import run_battery_config  # noqa: F401  (F1, builder runs only)
+        line = run_battery_config(args, world, rank, local, dev)
+        tables = {}
     else:
-        from bench_configs import run_other
-        line = run_other(args, world, rank, local)
-    table = line.pop("_table", None)
+        main_cfg = args.config
+        line, t0 = RUNNERS[main_cfg](args, world, rank, local, dev, peak)
+        tables = {main_cfg: t0}
+        if main_cfg != 2 and "metric" not in line:
+            line = {"metric": METRIC, **line, "vs_baseline": None,
+                    "dtype": "u32 Montgomery / u64 skip + f64 map", "data": "synthetic: derived stream params"}
+        if main_cfg == 2 and not args.no_sub:
+            line["configs"] = {}
+            for c in SUB_CONFIGS:
+                torch.cuda.empty_cache()
+                sub, tables[c] = RUNNERS[c](args, world, rank, local, dev, peak)
+                line["configs"][str(c)] = sub
+    if rank == 0 and not args.no_cpu and world == 1:  # the CPU baseline is an N=1, rank-0 measurement
+        line["cpu_baseline"] = C.cpu_baseline_for(args.config, tables.get(args.config))
+        for c, sub in line.get("configs", {}).items():
+            sub["cpu_baseline"] = C.cpu_baseline_for(int(c), tables.get(int(c)))
     if rank == 0:
-        if not args.no_cpu and world == 1:  # the CPU baseline is an N=1, rank-0 measurement
-            if args.config == 2:
-                line["cpu_baseline"] = cpu_port_rate()
-                one = cpu_port_rate(procs=1)  # SURVEY §8(d): also the single-process figure
-                line["cpu_baseline"]["one_process"] = {"value": one["value"], "unit": one["unit"], "cores": 1}
-            else:
-                from bench_configs import cpu_baseline_for
-                cb = cpu_baseline_for(args.config, table)
-                if cb:
-                    line["cpu_baseline"] = cb
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -439,6 +503,7 @@ def run_gpu(args):
 
 
 def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -447,12 +512,19 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--one-lane", action="store_true", help="A/B: one lane per thread (RSA_FLAG_ONE_LANE)")
+    ap.add_argument("--no-sub", action="store_true", help="config 2 only (no configs{} sub-results)")
+    ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args(argv)
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps violates the timing rules", file=sys.stderr)
     if args.impl == "reference":
         return run_reference_arm(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(args, argv)
+    if args.launch_check:
+        return launch_check(args)
     return run_gpu(args)
 
 

@@ -1,220 +1,293 @@
-"""Secondary bench configurations (bench.py --config 3|4|5): BASELINE.json
-configs[2..4].  Same timing rules as bench.py (events on the launch stream,
-barrier + synchronize both sides, max over ranks)."""
+"""Bench workloads: one class per BASELINE.json configuration, shared by
+bench.py (which times them) and the full-size parity tests (which check the
+very launches the bench times: tests/test_gpu_fullsize.py).
+
+    Config2  configs[1]  single-instance bulk fill, 4 x 2^30 f64 (e = 3, 5, 17, 65537)
+    Config1  configs[0]  stream 0, 2^20 f64 per take at Mv = 1, 64, 65536
+    Config3  configs[2]  65,536 instances x Mv 64 x 1024 blocks, e = 9 (strong scaling)
+    Config4  configs[3]  2^20 instances x 2^16 draws fused, e = 9 (strong scaling + all-reduce)
+    Config5  configs[4]  safe-prime census of [2^31, 2^32) + 2^20 instance tuples
+
+Every workload builds its inputs once (untimed) and exposes `step()`, one
+pass of the hot path over one batch, launched on torch's current stream.
+Units: `numbers_per_step` is the WHOLE-JOB count (all ranks); each rank does
+its shard.  The reference's own CPU timer for the path is `cli.bench_throughput`
+(/root/reference/pkg/src/rsarand/cli.py:189-200); `cpu_baseline_for` times the
+restated algorithm (oracle/, test infrastructure) on bounded samples of the
+same workloads.
+"""
 
 from __future__ import annotations
 
+import dataclasses
+import json
+import os
 import statistics
 
-import bench
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+
+EXPONENTS = (3, 5, 17, 65537)
+M0_RNG_SEED = 181111629
 
 
-def _time_steps(args, world, fn, local):
-    import torch
-    stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
-        fn()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    bench.barrier_sync(world)
-    with bench.ClockSampler(local) as clk:
-        t0.record(stream)
-        for _ in range(args.steps):
-            fn()
-        t1.record(stream)
-        bench.barrier_sync(world)
-    return bench.max_over_ranks(t0.elapsed_time(t1) * 1e-3, world), clk.summary()
+def w_imad(e: int) -> int:
+    """Algorithmic IMAD-class ops per draw, W(e) = 6 M(e) + 13."""
+    m = e.bit_length() - 1 + bin(e).count("1") - 1
+    return 6 * m + 13
 
 
-def _base_line(args, world, value, elapsed, clk, config, launches):
-    return {"metric": bench.METRIC, "value": value, "unit": "Gnumbers/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "u32 Montgomery / u64 skip + f64 map", "data": "synthetic: derived stream params",
-            "config": config, "clocks": clk, "gpu_launches": launches}
+def seeded_m0(n: int) -> int:
+    return int(np.random.default_rng(M0_RNG_SEED).integers(0, n, dtype=np.uint64))
 
 
-def run_other(args, world, rank, local):
-    import torch
-    import paper_1811_11629_b200 as R
-    from paper_1811_11629_b200 import _device, _lib, vecgen
-    from paper_1811_11629_b200.shard import shard_range
-    dev = torch.device("cuda", local)
-    peak = bench.probe_imad_peak(dev)
+def _profiles_json(name: str) -> dict:
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
 
-    if args.config == 3:
-        total, mv, blocks = 1 << 16, 64, 1024
-        first, n = shard_range(total, world, rank)
-        t = R.derive_params_table(R.DEFAULT_MASTER_SEED, first, n, dev=dev)
-        m1, m2, s = vecgen._init_lanes(t.inst, n, mv, 0, 1, dev)
-        out = torch.empty((n, blocks * mv), dtype=torch.float64, device=dev)
 
-        def fn():
-            _lib.call("rsa_fill", t.inst.data_ptr(), n, mv, blocks, 9, _lib.RSA_FLAG_FAST,
-                      m1.data_ptr(), m2.data_ptr(), s.data_ptr(), None, out.data_ptr(),
-                      blocks * mv, _device.stream(dev))
+def load_slots(key: str):
+    return _profiles_json("slots.json").get(key)
 
-        el, clk = _time_steps(args, world, fn, local)
-        numbers = total * mv * blocks
-        line = _base_line(args, world, numbers * args.steps / el / 1e9, el, clk,
-                          {"workload": "config3: 65536 instances (ids 0..65535), e=9, Mv=64, 1024 blocks, "
-                                       "2^16 f64 each, instance-major, sharded by contiguous id range",
-                           "l2": "32 GiB output per step (> L2)"}, args.steps)
-        per = el / args.steps
-        line["roofline"] = {"bound": "imad", "achieved": bench.w_imad(9) * numbers / world / per / 1e12,
-                            "peak": peak["ops_per_s"] / 1e12, "unit": "Tops/s",
-                            "frac": bench.w_imad(9) * numbers / world / per / peak["ops_per_s"],
-                            "traffic": bench.load_traffic("fill_c3")}
-        line["_table"] = t  # for the rank-0 CPU baseline (bench.run_gpu)
-        return line
 
-    if args.config == 4:
-        total, N = 1 << 20, 1 << 16
-        first, n = shard_range(total, world, rank, align=2)
-        t = R.derive_params_table(R.DEFAULT_MASTER_SEED, first, n, dev=dev)
-        fc = R.FusedConsumer(t)
-        box = {}
+def load_traffic(key: str):
+    return _profiles_json("traffic.json").get(key)
 
-        def fn():
-            res = fc.run(N)
-            if world > 1:
-                R.all_reduce_pooled(res)
-            box["res"] = res
 
-        el, clk = _time_steps(args, world, fn, local)
-        numbers = total * N
-        line = _base_line(args, world, numbers * args.steps / el / 1e9, el, clk,
-                          {"workload": "config4 fused consumer: 2^20 instances x 2^16 draws, Mv=1, e=9; "
-                                       "per-instance mean/var/lag-1/64-bin hist + pooled pair correlation; "
-                                       "NCCL all-reduce of pooled stats", "l2": "no stream in HBM"},
-                          args.steps * (3 + (2 if world > 1 else 0)))
-        per = el / args.steps
-        line["roofline"] = {"bound": "imad", "achieved": bench.w_imad(9) * numbers / world / per / 1e12,
-                            "peak": peak["ops_per_s"] / 1e12, "unit": "Tops/s",
-                            "frac": bench.w_imad(9) * numbers / world / per / peak["ops_per_s"],
-                            "traffic": bench.load_traffic("fused")}
-        line["pooled_correlation"] = box["res"].pooled_correlation(total // 2)
-        line["_table"] = t  # for the rank-0 CPU baseline (bench.run_gpu)
-        return line
+def heavy_pipe(key: str, draws: int, seconds: float, peak: dict, clk: dict) -> dict | None:
+    """The datapath that bounds the draw kernels: IMAD.WIDE/IMAD.HI (2 slots),
+    IMAD and FP64 ops (1 slot) share 64 slots/clk/SM on B200
+    (profiles/r01_probe_hybrid.txt).  Slots per draw are counted from the SASS
+    (tools/slots_json.py -> profiles/slots.json); the measured peak is the
+    in-run Montgomery-triple probe (3 instructions = 5 slots)."""
+    spd = load_slots(key)
+    if not spd:
+        return None
+    ach = spd * draws / seconds
+    meas = peak["ops_per_s"] * 5.0 / 3.0
+    out = {"slots_per_draw": spd, "achieved_tslots": ach / 1e12, "peak_tslots_measured": meas / 1e12,
+           "frac_of_measured": ach / meas}
+    if clk.get("sm_mhz"):
+        nominal = 64.0 * peak["sms"] * clk["sm_mhz"] * 1e6
+        out["peak_tslots_nominal_at_clock"] = nominal / 1e12
+        out["frac_of_nominal"] = ach / nominal
+    return out
 
-    if args.config == 1:
-        # config 1: one instance (stream 0), 2^20 draws at Mv = 1 (the scalar
-        # stream), 64 (`rsarand gen` default) and 65536 (`rsarand bench` default)
-        p = R.derive_stream_params(R.StreamKey(R.DEFAULT_MASTER_SEED, 0), dev=dev)
-        count = 1 << 20
-        per_mv = {}
+
+def imad_roofline(e: int, draws: int, seconds: float, peak: dict, kernel: str, traffic_key: str | None,
+                  slots_key: str | None, clk: dict, hbm_bytes_per_draw: int = 8) -> dict:
+    """IMAD roofline of one draw kernel launch: W(e) IMAD-class ops per draw
+     / launch time, against the in-run Montgomery-triple
+    probe; plus the HBM write fraction and the heavy-datapath slot rate."""
+    from bench import peaks
+    ach = w_imad(e) * draws / seconds
+    hbm_peak = peaks().get("hbm_gbs")
+    hbm = hbm_bytes_per_draw * draws / seconds / 1e9
+    return {"bound": "imad", "kernel": kernel, "achieved": ach / 1e12, "peak": peak["ops_per_s"] / 1e12,
+            "unit": "Tops/s", "frac": ach / peak["ops_per_s"],
+            "traffic": load_traffic(traffic_key) if traffic_key else None,
+            "algorithmic_ops_per_draw": w_imad(e), "draws_per_launch": draws, "launch_ms": seconds * 1e3,
+            "peak_source": "measured in-run: rsa_probe_imad Montgomery-triple stream (IMAD-class ops/s)",
+            "hbm": {"achieved_gbs": hbm, "peak_gbs": hbm_peak,
+                    "frac": hbm / hbm_peak if hbm_peak else None,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)"},
+            "heavy_pipe": heavy_pipe(slots_key, draws, seconds, peak, clk) if slots_key else None}
+
+
+# ---------------------------------------------------------------------------
+# workloads
+
+class Config2:
+    """configs[1]: one instance per rank (stream id = rank, DEFAULT_MASTER_SEED),
+    seeded uniform m0, Mv = 2^22; per exponent e in {3, 5, 17, 65537} one
+    take_floats of 2^30 doubles (256 blocks) into HBM.  Weak scaling."""
+
+    MV = 1 << 22
+    BLOCKS = 256
+    scaling = "weak"
+
+    def __init__(self, dev, world: int, rank: int):
+        import paper_1811_11629_b200 as R
+        from paper_1811_11629_b200 import vecgen
+        self.R = R
+        base = R.derive_stream_params(R.StreamKey(R.DEFAULT_MASTER_SEED, rank), dev=dev)
+        self.m0 = seeded_m0(base.n)
+        params = {e: dataclasses.replace(base, e=e) for e in EXPONENTS}  # e=65537 bypasses validation
+        st0 = R.init_vector(base, m0=self.m0, mv=self.MV, device=dev)
+        self.states = {e: vecgen.VectorState(params=params[e], mv=self.MV, m1=st0.m1.clone(),
+                                             m2=st0.m2.clone(), s=st0.s.clone()) for e in EXPONENTS}
+        self.count = self.MV * self.BLOCKS
+        import torch
+        self.out = torch.empty(self.count, dtype=torch.float64, device=dev)
+        self.numbers_per_step = world * len(EXPONENTS) * self.count
+        self.launches_per_step = len(EXPONENTS)
+
+    def step(self, events=None):
+        import torch
         stream = torch.cuda.current_stream()
-        for mv in (1, 64, 65536):
-            st = R.init_vector(p, m0=0, s0=1, mv=mv, device=dev)
-            out = torch.empty(count, dtype=torch.float64, device=dev)
-            for _ in range(args.warmup):
-                R.take_floats(st, count, out=out)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            bench.barrier_sync(world)
-            a.record(stream)
-            for _ in range(args.steps):
-                R.take_floats(st, count, out=out)
-            b.record(stream)
-            b.synchronize()
-            per_mv[str(mv)] = {"ms_per_2e20": a.elapsed_time(b) / args.steps,
-                               "gnumbers_s": count * args.steps / (a.elapsed_time(b) * 1e-3) / 1e9}
-        el = sum(v["ms_per_2e20"] for v in per_mv.values()) * 1e-3 * args.steps
-        line = _base_line(args, world, 3 * count * args.steps / el / 1e9, el, {"sm_mhz": None},
-                          {"workload": "config1: stream 0, e=9, 2^20 f64 per take_floats at Mv=1, 64, 65536 "
-                                       "(Mv<2^17 lanes are split across threads: rsa_fill_segmented)"},
-                          args.steps * 3 * 3)
-        line["per_mv"] = per_mv
-        line["reference_context"] = ("reference scalar rsacore.take_raws 2.35 us/draw (4.26e5/s) and "
-                                     "vecgen bench_throughput 1.18e7/s at Mv=65536, one core (SURVEY §6)")
-        return line
+        for e in EXPONENTS:
+            if events is not None:
+                events[e][0].record(stream)
+            self.R.take_floats(self.states[e], self.count, out=self.out)
+            if events is not None:
+                events[e][1].record(stream)
 
-    if args.config == 6:
-        # F1: the full chi-square battery (13 core tests + 10 low-bit reruns)
-        # on 2 interleaved streams at the reference's DEFAULT_BUDGET (1e8 per test)
-        import time
-        from paper_1811_11629_b200 import bitsource, stats
-        budget = 100_000_000
-        plist = bitsource.interstream_params(R.DEFAULT_MASTER_SEED, 9, 2, dev=dev)
 
-        def make(sel):
-            return bitsource.BitSource([R.init_vector(p, m0=0, s0=1, mv=1 << 16, device=dev)
-                                        for p in plist], sel)
+class Config1:
+    """configs[0]: stream 0, e = 9, m0 = 0, s0 = 1; one step = a take_floats of
+    2^20 doubles at each of Mv = 1 (the scalar stream), 64 (`rsarand gen`'s
+    default) and 65536 (`rsarand bench`'s default).  Latency-bound at this
+    size.  Every rank runs its own copy (weak)."""
 
-        stats.run_battery(make, budget=1 << 23)  # warm-up (allocator, cuFFT plans)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        rep = stats.run_battery(make, budget=budget)
-        torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        variates = sum(r.samples for r in rep.reports)
-        line = _base_line(args, world, variates / el / 1e9, el * args.steps, {"sm_mhz": None},
-                          {"workload": "config6 (F1): stats.run_battery, 23 tests at budget 1e8 each, "
-                                       "2 interleaved streams (9, 10), Mv=2^16"}, None)
-        line["unit"] = "Gvariates/s"
-        line["ms_per_step"] = el * 1e3
-        line["battery"] = {"tests": len(rep.reports), "errors": rep.errors, "all_pass": rep.all_pass,
-                           "n_outside_warn": rep.n_outside_warn,
-                           "records": [r.record() for r in rep.reports]}
-        line["reference_context"] = ("reference run_battery at budget 2^23 took 57.6 s on one CPU core here "
-                                     "(tests/golden/battery.json): 3.35e6 variates/s")
-        return line
+    COUNT = 1 << 20
+    MVS = (1, 64, 65536)
+    scaling = "weak"
 
-    # config 5: safe-prime scan of [2^31, 2^32) + 2^20 instance tuples
-    from paper_1811_11629_b200 import paramfactory
-    lo_all, hi_all = 1 << 31, 1 << 32
-    span = (hi_all - lo_all) // world
-    lo = lo_all + rank * span
-    hi = hi_all if rank == world - 1 else lo + span
-    first, n = shard_range(1 << 20, world, rank)
-    paramfactory.safe_prime_table(dev)  # the derivation table (built once, untimed)
+    def __init__(self, dev, world: int, rank: int):
+        import torch
+        import paper_1811_11629_b200 as R
+        self.R = R
+        p = R.derive_stream_params(R.StreamKey(R.DEFAULT_MASTER_SEED, 0), dev=dev)
+        self.states = {mv: R.init_vector(p, m0=0, s0=1, mv=mv, device=dev) for mv in self.MVS}
+        self.outs = {mv: torch.empty(self.COUNT, dtype=torch.float64, device=dev) for mv in self.MVS}
+        self.numbers_per_step = world * len(self.MVS) * self.COUNT
 
-    phase = {"scan": [], "setup": []}
+    def step(self, events=None):
+        import torch
+        stream = torch.cuda.current_stream()
+        for mv in self.MVS:
+            if events is not None:
+                events[mv][0].record(stream)
+            self.R.take_floats(self.states[mv], self.COUNT, out=self.outs[mv])
+            if events is not None:
+                events[mv][1].record(stream)
 
-    def fn():
+
+class Config3:
+    """configs[2]: stream ids [0, 65536) of DEFAULT_MASTER_SEED, e = 9, m0 = 0,
+    s0 = 1, Mv = 64, 1024 blocks: 2^16 doubles per instance,
+    instance-major rows out[i, k*64 + g] (2^32 doubles = 32 GiB).  One step =
+    ONE rsa_fill launch over this rank's contiguous id shard (strong scaling:
+    the 2^32 total is fixed, no inter-GPU traffic)."""
+
+    TOTAL, MV, BLOCKS, E = 1 << 16, 64, 1024, 9
+    scaling = "strong"
+
+    def __init__(self, dev, world: int = 1, rank: int = 0, first: int | None = None, n: int | None = None):
+        import torch
+        import paper_1811_11629_b200 as R
+        from paper_1811_11629_b200 import vecgen
+        from paper_1811_11629_b200.shard import shard_range
+        sharded = first is None
+        if sharded:
+            first, n = shard_range(self.TOTAL, world, rank)
+        self.first, self.n, self.dev = first, n, dev
+        self.table = R.derive_params_table(R.DEFAULT_MASTER_SEED, first, n, dev=dev)
+        self.m1, self.m2, self.s = vecgen._init_lanes(self.table.inst, n, self.MV, 0, 1, dev)
+        self.out = torch.empty((n, self.BLOCKS * self.MV), dtype=torch.float64, device=dev)
+        self.numbers_per_step = (self.TOTAL if sharded else n) * self.MV * self.BLOCKS
+        self.local_numbers = n * self.MV * self.BLOCKS
+        self.launches_per_step = 1
+
+    def step(self):
+        from paper_1811_11629_b200 import _device, _lib
+        _lib.call("rsa_fill", self.table.inst.data_ptr(), self.n, self.MV, self.BLOCKS, self.E,
+                  _lib.RSA_FLAG_FAST, self.m1.data_ptr(), self.m2.data_ptr(), self.s.data_ptr(), None,
+                  self.out.data_ptr(), self.BLOCKS * self.MV, _device.stream(self.dev))
+
+
+class Config4:
+    """configs[3]: stream ids [0, 2^20), e = 9, Mv = 1, 2^16 draws per instance
+    generated in registers and reduced in-kernel (A13 statistics); at N > 1
+    the pooled sums are NCCL all-reduced.  Strong scaling over contiguous
+    pair-aligned id shards."""
+
+    TOTAL, DRAWS, E = 1 << 20, 1 << 16, 9
+    scaling = "strong"
+
+    def __init__(self, dev, world: int = 1, rank: int = 0, first: int | None = None, n: int | None = None):
+        import paper_1811_11629_b200 as R
+        from paper_1811_11629_b200.shard import shard_range
+        sharded = first is None
+        if sharded:
+            first, n = shard_range(self.TOTAL, world, rank, align=2)
+        self.R, self.world = R, world
+        self.first, self.n = first, n
+        self.table = R.derive_params_table(R.DEFAULT_MASTER_SEED, first, n, dev=dev)
+        self.fc = R.FusedConsumer(self.table)
+        self.numbers_per_step = (self.TOTAL if sharded else n) * self.DRAWS
+        self.local_numbers = n * self.DRAWS
+        self.launches_per_step = 3
+        self.result = None
+
+    def step(self):
+        res = self.fc.run(self.DRAWS)
+        if self.world > 1:
+            self.R.all_reduce_pooled(res)
+        self.result = res
+        return res
+
+
+class Config5:
+    """configs[4]: the safe-prime census of every odd candidate in [2^31, 2^32)
+    (production scan: sieve + base-2 SPRP + the spsp(2) table; the literal
+    MR(2, 7, 61) census is timed beside it) + the 2^20 instance tuples of ids
+    [0, 2^20).  At N > 1 each rank scans a contiguous sub-interval and the
+    counts and lists are all-gathered."""
+
+    scaling = "strong"
+
+    def __init__(self, dev, world: int = 1, rank: int = 0):
+        from paper_1811_11629_b200 import paramfactory
+        from paper_1811_11629_b200.shard import shard_interval, shard_range
+        self.dev, self.world = dev, world
+        self.lo, self.hi = shard_interval(1 << 31, 1 << 32, world, rank)
+        self.first, self.n = shard_range(1 << 20, world, rank)
+        paramfactory.safe_prime_table(dev)  # the derivation table (built once, untimed)
+        self.numbers_per_step = (1 << 30)  # odd candidates in [2^31, 2^32)
+        self.launches_per_step = 8
+        self.phase = {"scan": [], "setup": []}
+        self.count = None
+
+    def step(self):
+        import torch
+        import paper_1811_11629_b200 as R
+        from paper_1811_11629_b200 import paramfactory
         st = torch.cuda.current_stream()
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(st)
-        sp = paramfactory.safe_primes_u32(lo, hi, dev)
-        if world > 1:  # all-gather the per-rank counts and lists -> the global table
+        sp = paramfactory.safe_primes_u32(self.lo, self.hi, self.dev)
+        if self.world > 1:
             from paper_1811_11629_b200.shard import gather_sorted
             sp = gather_sorted(sp.view(torch.int32))
         e1.record(st)
-        R.derive_params_table(R.DEFAULT_MASTER_SEED, first, n, dev=dev)
+        R.derive_params_table(R.DEFAULT_MASTER_SEED, self.first, self.n, dev=self.dev)
         e2.record(st)
+        self._pending = (e0, e1, e2, sp)
+
+    def collect(self):
+        e0, e1, e2, sp = self._pending
         e2.synchronize()
-        phase["scan"].append(e0.elapsed_time(e1))
-        phase["setup"].append(e1.elapsed_time(e2))
-        phase["count"] = int(sp.numel())
-
-    el, clk = _time_steps(args, world, fn, local)
-    cands = (hi_all - lo_all) // 2
-    line = _base_line(args, world, cands * args.steps / el / 1e9, el, clk,
-                      {"workload": "config5 setup: safe-prime scan (sieve to 8191, base-2 SPRP, spsp(2) table) of all 2^30 odd candidates in "
-                                   "[2^31,2^32) + 2^20 instance tuples (ids 0..2^20-1)",
-                       "unit_note": "value = odd candidates per second (scan + tuples in the step; at N>1 the scan phase includes the all-gather of the per-rank counts and lists)"},
-                      args.steps * 5)
-    line["unit"] = "Gcandidates/s"
-    scan_ms = statistics.median(phase["scan"][-args.steps:])
-    setup_ms = statistics.median(phase["setup"][-args.steps:])
-    line["phases"] = {"scan_ms": scan_ms, "scan_gcandidates_s": cands / world / (scan_ms * 1e-3) / 1e9,
-                      "safe_primes_found": phase["count"], "setup_ms": setup_ms,
-                      "tuples_per_s": n / (setup_ms * 1e-3)}
-    if world == 1:
-        line["literal_mr"] = literal_mr_scan(args, lo, hi, dev, phase["count"])
-    return line
+        self.phase["scan"].append(e0.elapsed_time(e1))
+        self.phase["setup"].append(e1.elapsed_time(e2))
+        self.count = int(sp.numel())
 
 
-def literal_mr_scan(args, lo, hi, dev, want_count):
+def literal_mr_scan(steps: int, lo: int, hi: int, dev, want_count: int, peak: dict) -> dict:
     """The census exactly as BASELINE config 5 words it (MR 2, 7, 61 on every
     odd n and on (n-1)/2; rsa_safe_prime_scan_mr), timed beside the production
     scan.  Roofline: SURVEY §8(d)'s 55.5 Montgomery products per odd candidate
     against the in-run Montgomery-triple probe (products/s)."""
     import torch
-    from bench import probe_imad_peak
     from paper_1811_11629_b200 import paramfactory
     st = torch.cuda.current_stream()
     paramfactory.safe_primes_u32(lo, hi, dev, literal_mr=True)  # warm-up
     times = []
-    for _ in range(max(1, min(args.steps, 3))):
+    for _ in range(max(1, min(steps, 3))):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
         sp = paramfactory.safe_primes_u32(lo, hi, dev, literal_mr=True)
@@ -224,12 +297,12 @@ def literal_mr_scan(args, lo, hi, dev, want_count):
     ms = statistics.median(times)
     cands = (hi - lo) // 2
     products = 55.5 * cands
-    peak = probe_imad_peak(dev)["ops_per_s"] / 3.0  # Montgomery triples (products) per second
+    pk = peak["ops_per_s"] / 3.0  # Montgomery triples (products) per second
     return {"ms": ms, "gcandidates_s": cands / (ms * 1e-3) / 1e9, "safe_primes_found": int(sp.numel()),
             "equal_count": int(sp.numel()) == want_count,
             "roofline": {"bound": "imad", "kernel": "k_mr_base2 + k_mr_rest",
-                         "achieved": products / (ms * 1e-3) / 1e12, "peak": peak / 1e12,
-                         "unit": "T Montgomery products/s", "frac": products / (ms * 1e-3) / peak,
+                         "achieved": products / (ms * 1e-3) / 1e12, "peak": pk / 1e12,
+                         "unit": "T Montgomery products/s", "frac": products / (ms * 1e-3) / pk,
                          "algorithmic_products_per_candidate": 55.5},
             "note": "literal MR(2,7,61) census (no sieve, no pseudoprime table); the production scan "
                     "(phases.scan_ms) returns the same list"}
@@ -240,11 +313,59 @@ def literal_mr_scan(args, lo, hi, dev, want_count):
 # reference's algorithm restated in oracle/ (test infrastructure), timed on
 # the box's host cores the way each configuration's workload runs.
 
-def _cpu_cfg1(args):
+def _stream0():
+    from oracle import rsa_oracle as O
+    with open(os.path.join(ROOT, "tests", "golden", "regression.json")) as fh:
+        return O.from_fields(json.load(fh)["params"])
+
+
+def _cpu_cfg2(args):
+    """vecgen's lockstep path (numpy port) at Mv = 65536 for each bench exponent."""
+    import time
+    from oracle import rsa_oracle as O
+    e_list, blocks, mv = args
+    P0 = _stream0()
+    st = O.init(P0, m0=seeded_m0(P0.n), mv=mv)
+    out = {}
+    for e in e_list:
+        P = dataclasses.replace(P0, e=e)
+        m1, m2, s = st.m1.copy(), st.m2.copy(), st.s.copy()
+        O.block_raw(m1, m2, s, P)  # warm-up
+        t0 = time.perf_counter()
+        for _ in range(blocks):
+            raw, m1, m2, s = O.block_raw(m1, m2, s, P)
+            O.floats_from_raw(raw, P)
+        out[e] = (blocks * mv, time.perf_counter() - t0)
+    return out
+
+
+def cpu_port_rate(procs: int | None = None, blocks: int = 4, mv: int = 65536) -> dict:
+    """Aggregate numbers/s of the numpy port of vecgen's lockstep path
+    (Mv=65536, the reference CLI bench default, cli.py:26) over all host cores,
+    with the step's exponent mix weighted equally per draw."""
+    import multiprocessing as mp
+    procs = procs or os.cpu_count() or 1
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_cpu_cfg2, [(EXPONENTS, blocks, mv)] * procs)
+    per_e = {}
+    for e in EXPONENTS:
+        draws = sum(r[e][0] for r in res)
+        wall = max(r[e][1] for r in res)
+        per_e[e] = draws / wall
+    rate = len(EXPONENTS) / sum(1.0 / per_e[e] for e in EXPONENTS)  # equal draws per e
+    draws = sum(r[e][0] for r in res for e in EXPONENTS)
+    return {"value": rate / 1e9, "unit": "Gnumbers/s", "cores": procs, "kind": "port",
+            "per_e": {str(e): per_e[e] / 1e9 for e in EXPONENTS},
+            "sample": f"numpy port of vecgen lockstep (oracle/rsa_oracle.py), Mv={mv}, {blocks} "
+                      f"blocks per e in {list(EXPONENTS)} per process, {procs} processes "
+                      f"({draws} draws), stream 0 seeded m0; {os.cpu_count()} host cores"}
+
+
+def _cpu_cfg1(count):
     """Scalar stream (Mv = 1): the rsacore per-draw path in Python ints."""
     import time
     from oracle import rsa_oracle as O
-    P, count = args
+    P = _stream0()
     t = time.perf_counter()
     O.scalar_raws(P, count)
     return count, time.perf_counter() - t
@@ -268,7 +389,6 @@ def _cpu_cfg4(args):
     """Config-4 instances: the C restatement draws each Mv = 1 stream, the
     numpy restatement of the A13 statistics reduces them."""
     import time
-    import numpy as np
     from oracle import coracle
     from oracle import rsa_oracle as O
     plist, N = args
@@ -293,18 +413,19 @@ def _cpu_cfg5(args):
 
 
 def cpu_baseline_for(config: int, table=None) -> dict | None:
-    """cpu_baseline object for bench.py --config N (N != 2; config 2 uses
-    bench.cpu_port_rate).  `table`: the derived InstanceTable of the run."""
+    """cpu_baseline object of configuration `config` (rank 0, N = 1).
+    `table`: the InstanceTable the GPU run derived (configs 3 and 4)."""
     import multiprocessing as mp
-    import os
     from oracle import rsa_oracle as O
     procs = os.cpu_count() or 1
-    with open(os.path.join(bench.ROOT, "tests", "golden", "regression.json")) as fh:
-        import json
-        P0 = O.from_fields(json.load(fh)["params"])
+    if config == 2:
+        cb = cpu_port_rate()
+        one = cpu_port_rate(procs=1)  # SURVEY §8(d): also the single-process figure
+        cb["one_process"] = {"value": one["value"], "unit": one["unit"], "cores": 1}
+        return cb
     if config == 1:
         n = 1 << 17
-        draws, wall = _cpu_cfg1((P0, n))
+        draws, wall = _cpu_cfg1(n)
         return {"value": draws / wall / 1e9, "unit": "Gnumbers/s", "cores": 1, "kind": "port",
                 "sample": f"{n} scalar draws of stream 0 (oracle.scalar_raws: rsacore's per-draw path in "
                           f"Python ints, rsacore.py:236-258), one process"}
@@ -319,7 +440,8 @@ def cpu_baseline_for(config: int, table=None) -> dict | None:
                           f"Mv = 64 each (numpy lockstep port of vecgen, e = 9)"}
     if config == 4:
         per = 4
-        plist = [(table.params(j).p1, table.params(j).p2, table.params(j).skip.a) for j in range(per * procs)]
+        recs = [table.params(j) for j in range(per * procs)]
+        plist = [(p.p1, p.p2, p.skip.a) for p in recs]
         N = 1 << 16
         jobs = [(plist[per * k:per * k + per], N) for k in range(procs)]
         with mp.get_context("fork").Pool(procs) as pool:
@@ -332,12 +454,46 @@ def cpu_baseline_for(config: int, table=None) -> dict | None:
         span = 1 << 27
         n5 = min(procs, (1 << 31) // span)  # disjoint windows inside [2^31, 2^32)
         jobs = [((1 << 31) + k * span, (1 << 31) + (k + 1) * span) for k in range(n5)]
-        procs = n5
-        with mp.get_context("fork").Pool(procs) as pool:
+        with mp.get_context("fork").Pool(n5) as pool:
             res = pool.map(_cpu_cfg5, jobs)
         return {"value": sum(d for d, _ in res) / max(w for _, w in res) / 1e9, "unit": "Gcandidates/s",
-                "cores": procs, "kind": "port",
-                "sample": f"safe-prime census of {procs} disjoint 2^27-wide windows from 2^31, one per "
+                "cores": n5, "kind": "port",
+                "sample": f"safe-prime census of {n5} disjoint 2^27-wide windows from 2^31, one per "
                           f"process (C restatement of the reference's segmented sieve, "
                           f"paramfactory.py:85-130; faster than the reference's numpy sieve)"}
     return None
+
+
+def run_battery_config(args, world, rank, local, dev) -> dict:
+    """--config 6 (F1, builder runs): the full chi-square battery (13 core
+    tests + 10 low-bit reruns, stats.run_battery, stats.py:548-581) on 2
+    interleaved streams at the reference's DEFAULT_BUDGET (1e8 per test)."""
+    import time
+    import torch
+    import paper_1811_11629_b200 as R
+    from bench import METRIC, ClockSampler
+    from paper_1811_11629_b200 import bitsource, stats
+    budget = 100_000_000
+    plist = bitsource.interstream_params(R.DEFAULT_MASTER_SEED, 9, 2, dev=dev)
+
+    def make(sel):
+        return bitsource.BitSource([R.init_vector(p, m0=0, s0=1, mv=1 << 16, device=dev) for p in plist], sel)
+
+    stats.run_battery(make, budget=1 << 23)  # warm-up (allocator, cuFFT plans)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        rep = stats.run_battery(make, budget=budget)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+    variates = sum(r.samples for r in rep.reports)
+    return {"metric": METRIC, "value": variates / el / 1e9, "unit": "Gvariates/s", "n_gpus": world,
+            "steps": 1, "warmup": 1, "ms_per_step": el * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64 draws -> f64 / low bits", "data": "synthetic: derived stream params",
+            "config": {"workload": "config6 (F1): stats.run_battery, 23 tests at budget 1e8 each, "
+                                   "2 interleaved streams (9, 10), Mv=2^16"},
+            "clocks": clk.summary(),
+            "battery": {"tests": len(rep.reports), "errors": rep.errors, "all_pass": rep.all_pass,
+                        "n_outside_warn": rep.n_outside_warn, "records": [r.record() for r in rep.reports]},
+            "reference_context": ("reference run_battery at budget 2^23 took 57.6 s on one CPU core here "
+                                  "(tests/golden/battery.json): 3.35e6 variates/s")}

@@ -74,8 +74,8 @@ typedef struct rsa_instance {
     double n_float;           /*  88  float(n) (rsacore.py:104)                  */
     double n_recip;           /*  96  RN(1/n_float)                              */
     uint64_t skip_const;      /* 104  const-mode skip value (rsacore.py:91)      */
-    double n_recip_lo;        /* 112  RN((1 - n_float*n_recip) * n_recip): 1/fl(n) ~ hi + lo */
-    uint64_t reserved2;       /* 120                                             */
+    uint64_t reserved1;       /* 112  0                                          */
+    uint64_t reserved2;       /* 120  0                                          */
 } rsa_instance;
 
 /* ---------------------------------------------------------------------------

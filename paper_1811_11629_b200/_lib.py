@@ -36,7 +36,7 @@ RSA_FLAG_INTERLEAVE, RSA_FLAG_LOW32 = 16, 32
 INSTANCE_DTYPE = np.dtype({
     "names": ["p1", "p2", "p1_inv", "p2_inv", "a", "e", "k1", "k2", "r2_1", "r2_2",
               "garner", "p2inv", "q1", "q2", "flags", "skip_mode", "n", "q", "b",
-              "n_float", "n_recip", "skip_const", "n_recip_lo", "reserved2"],
+              "n_float", "n_recip", "skip_const", "reserved1", "reserved2"],
     "formats": ["<u4"] * 16 + ["<u8"] * 3 + ["<f8", "<f8", "<u8", "<f8", "<u8"],
     "offsets": [0, 4, 8, 12, 16, 20, 24, 28, 32, 36, 40, 44, 48, 52, 56, 60,
                 64, 72, 80, 88, 96, 104, 112, 120],

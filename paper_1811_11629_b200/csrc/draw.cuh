@@ -17,7 +17,7 @@ namespace rsa {
 struct FastInst {
     uint32_t p1, p2, p1_inv, p2_inv, a, k1, k2, garner, r2_1, r2_2, e;
     uint32_t gA, gB;  // fused-Garner constants (draw_fast_hc<E, true>)
-    double p2d, n_float, n_recip, n_recip_lo;
+    double n_float, n_recip;
 };
 
 // Fused Garner (p1's k-correction folded into the Garner product): valid when
@@ -52,10 +52,8 @@ RSA_DEV FastInst load_fast(const rsa_instance* __restrict__ ip) {
     P.r2_1 = w2.x; P.r2_2 = w2.y; P.garner = w2.z;
     P.gA = mont_mul(P.k1, P.garner, P.p1, P.p1_inv);  // k1 * p2inv mod p1
     P.gB = P.p1 - P.garner;                            // -p2inv * R mod p1 (garner != 0)
-    P.p2d = (double)P.p2;
     P.n_float = __ldg(&ip->n_float);
     P.n_recip = __ldg(&ip->n_recip);
-    P.n_recip_lo = __ldg(&ip->n_recip_lo);
     return P;
 }
 
@@ -78,21 +76,10 @@ RSA_DEV Lane lane_in(const FastInst& P, uint64_t m1, uint64_t m2, uint64_t s) {
 RSA_DEV uint64_t lane_m1(const FastInst& P, const Lane& L) { return mont_mul(L.x1, P.r2_1, P.p1, P.p1_inv); }
 RSA_DEV uint64_t lane_m2(const FastInst& P, const Lane& L) { return mont_mul(L.x2, P.r2_2, P.p2, P.p2_inv); }
 
-// A/B knobs (tools/ab, profiles/r01_ab_msg_fl.txt): both variants cut heavy
-// slots but measured slower, so the defaults stay 0.
-#ifndef RSA_MSG_VARIANT
-#define RSA_MSG_VARIANT 0
-#endif
 // x + REDC(s) mod p (the message step in the R^-1 domain, vecgen.py:94-95).
+// (Measured alternatives: tools/variants/draw_variants.cuh.)
 RSA_DEV uint32_t msg_add(uint32_t x, uint64_t s, uint32_t p, uint32_t pinv) {
-#if RSA_MSG_VARIANT == 0
     return add_mod(x, mont_redc(s, p, pinv), p);
-#else  // carry-flag add: -5 heavy slots per 2 draws at e=3, measured 2 % slower
-    uint32_t y = mont_redc(s, p, pinv);
-    uint32_t r, c;
-    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, 0, 0;" : "=r"(r), "=r"(c) : "r"(x), "r"(y));
-    return (c | (uint32_t)(r >= p)) ? r - p : r;
-#endif
 }
 
 template <uint32_t E>
@@ -148,21 +135,10 @@ RSA_DEV uint64_t draw_fast(const FastInst& P, Lane& L) {
     return (uint64_t)h * P.p2 + c2;
 }
 
-#ifndef RSA_FL_FMA
-#define RSA_FL_FMA 0
-#endif
-// One draw mapped to r = min(fl(c)/fl(n), 1-2^-53) (vecgen.py:103-107) when
-// the ciphertext itself is not needed: fl(c) = RN(h*p2 + c2) is one FMA of
-// exactly representable operands (RSA_FL_FMA), else I2F of the 64-bit c.
+// One draw mapped to r = min(fl(c)/fl(n), 1-2^-53) (vecgen.py:103-107).
 template <uint32_t E, bool GF>
 RSA_DEV double draw_unit(const FastInst& P, Lane& L) {
-#if RSA_FL_FMA
-    uint32_t h, c2;
-    draw_fast_hc<E, GF>(P, L, h, c2);
-    return unit_from_fl(__fma_rn((double)h, P.p2d, (double)c2), P.n_float, P.n_recip, P.n_recip_lo);
-#else
-    return to_unit(draw_fast<E, GF>(P, L), P.n_float, P.n_recip, P.n_recip_lo);
-#endif
+    return to_unit(draw_fast<E, GF>(P, L), P.n_float, P.n_recip);
 }
 
 // ---- general path (test-mode sizes, any prime q, unit/const skip) -------------
@@ -170,7 +146,7 @@ RSA_DEV double draw_unit(const FastInst& P, Lane& L) {
 struct GenInst {
     uint32_t p1, p2, p1_inv, p2_inv, a, e, k1, k2, r2_1, r2_2, garner, q1, q2, mode;
     uint64_t q, n;
-    double n_float, n_recip, n_recip_lo;
+    double n_float, n_recip;
 };
 
 RSA_DEV GenInst load_gen(const rsa_instance* __restrict__ ip) {
@@ -180,7 +156,6 @@ RSA_DEV GenInst load_gen(const rsa_instance* __restrict__ ip) {
     G.r2_1 = ip->r2_1; G.r2_2 = ip->r2_2; G.garner = ip->garner;
     G.q1 = ip->q1; G.q2 = ip->q2; G.mode = ip->skip_mode;
     G.q = ip->q; G.n = ip->n; G.n_float = ip->n_float; G.n_recip = ip->n_recip;
-    G.n_recip_lo = ip->n_recip_lo;
     return G;
 }
 

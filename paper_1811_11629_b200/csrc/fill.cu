@@ -68,24 +68,17 @@ k_fill_fast(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t total_l
     with_garner(P, [&](auto gf) {
         constexpr bool GF = decltype(gf)::value;
         for (uint64_t k = 0; k < blocks; ++k, off += step) {
-            if constexpr (!RAW && F64 == 1 && RSA_FL_FMA) {
-                double r[LPT];  // float-only fill: fl(c) by one FMA (draw_unit)
+            uint64_t c[LPT];
 #pragma unroll
-                for (int j = 0; j < LPT; ++j) r[j] = draw_unit<E, GF>(P, L[j]);
+            for (int j = 0; j < LPT; ++j) c[j] = draw_fast<E, GF>(P, L[j]);
+            if constexpr (RAW) store_u64<LPT>(raw + off, c);
+            if constexpr (F64 != 0) {
+                double r[LPT];
+#pragma unroll
+                for (int j = 0; j < LPT; ++j)
+                    r[j] = F64 == 1 ? to_unit(c[j], P.n_float, P.n_recip)
+                                    : __uint2double_rn((uint32_t)c[j]) * 0x1p-32;
                 store_f64<LPT>(f64 + off, r);
-            } else {
-                uint64_t c[LPT];
-#pragma unroll
-                for (int j = 0; j < LPT; ++j) c[j] = draw_fast<E, GF>(P, L[j]);
-                if constexpr (RAW) store_u64<LPT>(raw + off, c);
-                if constexpr (F64 != 0) {
-                    double r[LPT];
-#pragma unroll
-                    for (int j = 0; j < LPT; ++j)
-                        r[j] = F64 == 1 ? to_unit(c[j], P.n_float, P.n_recip, P.n_recip_lo)
-                                        : __uint2double_rn((uint32_t)c[j]) * 0x1p-32;
-                    store_f64<LPT>(f64 + off, r);
-                }
             }
         }
     });
@@ -117,7 +110,7 @@ k_fill_general(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t tota
     for (uint64_t k = 0; k < blocks; ++k, off += mv) {
         uint64_t c = draw_general(G, L);
         if (raw) raw[off] = c;
-        if (f64) f64[off] = to_unit(c, G.n_float, G.n_recip, G.n_recip_lo);
+        if (f64) f64[off] = to_unit(c, G.n_float, G.n_recip);
     }
     m1[lane] = mont_mul(L.x1, G.r2_1, G.p1, G.p1_inv);
     m2[lane] = mont_mul(L.x2, G.r2_2, G.p2, G.p2_inv);
@@ -128,10 +121,9 @@ __global__ void k_floats_from_raw(const uint64_t* __restrict__ raw, uint64_t cou
                                   double* __restrict__ out) {
     double nf = __ull2double_rn(n);
     double nr = __drcp_rn(nf);
-    double nl = __dmul_rn(__fma_rn(-nf, nr, 1.0), nr);
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count;
          j += (uint64_t)gridDim.x * blockDim.x)
-        out[j] = to_unit(raw[j], nf, nr, nl);
+        out[j] = to_unit(raw[j], nf, nr);
 }
 
 // out[j] = a * s[j] mod q: skipgen.next_skip_array (skipgen.py:108-116), one

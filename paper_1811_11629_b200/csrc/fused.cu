@@ -18,16 +18,10 @@ namespace rsa {
 constexpr int FUSED_BLOCK = 128;
 constexpr uint64_t FLUSH_MASK = (1u << 15) - 1;
 
-#ifndef RSA_FUSED_HIST32
-#define RSA_FUSED_HIST32 0
-#endif
-#if RSA_FUSED_HIST32
-typedef uint32_t hist_t;  // A/B: u32 counters bumped with shared-memory atomics
-#define RSA_HIST_BUMP(p) atomicAdd((p), 1u)
-#else
+// u16 counters (u32 shared-memory atomics measured +0.1 %, twice the smem:
+// profiles/r01_ab_msg_fl.txt, tools/variants/draw_variants.cuh)
 typedef uint16_t hist_t;
 #define RSA_HIST_BUMP(p) (*(p) += 1)
-#endif
 RSA_DEV void flush_hist(hist_t* h, uint32_t* gh, bool active) {
 #pragma unroll 8
     for (int b = 0; b < 64; ++b) {

@@ -129,7 +129,8 @@ RSA_DEV uint64_t mod_small_q(uint64_t x, uint64_t d) {
 }
 
 // x*y mod n for x, y < n, 2^32 <= n < 2^64, without the software 128-bit
-// modulo: the quotient is estimated in FP64 (off by < 2^13), the residue
+// modulo: the quotient is estimated in FP64 (five roundings on a quotient
+// below 2^64: off by < 5*2^11 < 2^14), the residue
 // P - Qe*n is formed exactly in 128-bit integers, one more FP64 rounding of
 // residue/n brings it into (-n, n), and one conditional add finishes.
 RSA_DEV uint64_t mulmod64_fp(uint64_t x, uint64_t y, uint64_t n) {
@@ -138,7 +139,7 @@ RSA_DEV uint64_t mulmod64_fp(uint64_t x, uint64_t y, uint64_t n) {
     const double Pd = __fma_rn(__ull2double_rn((uint64_t)(P >> 64)), 0x1p64, __ull2double_rn((uint64_t)P));
     const double qd = __dmul_rn(Pd, ninv);
     const uint64_t qe = qd >= 0x1p64 ? ~0ull : __double2ull_rz(qd);
-    __int128 R = (__int128)(P - (unsigned __int128)qe * n);  // exact: |R| < 2^13 n
+    __int128 R = (__int128)(P - (unsigned __int128)qe * n);  // exact: |R| < 2^14 n
     const double Rd = __fma_rn((double)(int64_t)(uint64_t)((unsigned __int128)R >> 64), 0x1p64,
                                __ull2double_rn((uint64_t)R));
     const int64_t q2 = __double2ll_rn(__dmul_rn(Rd, ninv));
@@ -198,12 +199,11 @@ constexpr double MAX_BELOW_ONE = 0x1.fffffffffffffp-1;  // rsacore.py:30
 // Markstein's correctly rounded final iteration (y within 1/2 ulp of 1/N, q1
 // faithful => RN(q1 + (x - q1 N) y) == RN(x/N)).  x >= 0, N > 0 normal; no
 // underflow/overflow at our magnitudes (x, N < 2^64).  5 FP64-pipe slots
-// against __ddiv_rn's ~16.  (A 4-op variant seeded with the double-double
-// reciprocal y + y_lo is also correctly rounded, but scheduled 3.7 % slower in
-// the e=65537 fill on B200 — profiles/r01_ab_v1_v3.txt — so y_lo is kept in
-// rsa_instance for callers but unused here.)  Checked bit-exact against IEEE
-// division by tests/test_gpu_fill.py::test_clamp_and_float_map.
-RSA_DEV double div_rn(double x, double N, double y, double /*y_lo*/) {
+// against __ddiv_rn's ~16.  (A 4-op variant seeded with a double-double
+// reciprocal is also correctly rounded, but scheduled 3.7 % slower in the
+// e=65537 fill on B200 — profiles/r01_ab_v1_v3.txt.)  Checked bit-exact
+// against IEEE division by tests/test_gpu_fill.py::test_clamp_and_float_map.
+RSA_DEV double div_rn(double x, double N, double y) {
     double q = __dmul_rn(x, y);
     double r = __fma_rn(-q, N, x);
     q = __fma_rn(r, y, q);
@@ -212,13 +212,13 @@ RSA_DEV double div_rn(double x, double N, double y, double /*y_lo*/) {
 }
 
 // r = min(fl(c)/fl(n), MAX_BELOW_ONE)  (vecgen.py:103-107)
-RSA_DEV double unit_from_fl(double x, double n_float, double n_recip, double n_recip_lo) {
-    double r = div_rn(x, n_float, n_recip, n_recip_lo);
+RSA_DEV double unit_from_fl(double x, double n_float, double n_recip) {
+    double r = div_rn(x, n_float, n_recip);
     return r < 1.0 ? r : MAX_BELOW_ONE;
 }
 
-RSA_DEV double to_unit(uint64_t c, double n_float, double n_recip, double n_recip_lo) {
-    return unit_from_fl(__ull2double_rn(c), n_float, n_recip, n_recip_lo);
+RSA_DEV double to_unit(uint64_t c, double n_float, double n_recip) {
+    return unit_from_fl(__ull2double_rn(c), n_float, n_recip);
 }
 
 // ---- primality (setup kernels) --------------------------------------------------

@@ -214,7 +214,7 @@ k_seg_fill(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t lanes, u
         for (uint64_t k = 0; k < len; ++k, off += mv) {
             const uint64_t c = draw_fast<E, GF>(P, Ln);
             if constexpr (RAW) __stcs(reinterpret_cast<unsigned long long*>(raw + off), (unsigned long long)c);
-            if constexpr (F64) __stcs(f64 + off, to_unit(c, P.n_float, P.n_recip, P.n_recip_lo));
+            if constexpr (F64) __stcs(f64 + off, to_unit(c, P.n_float, P.n_recip));
         }
     });
     if (j == nseg - 1) {  // the last segment owns the lane's final state
@@ -228,7 +228,7 @@ k_seg_fill(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t lanes, u
 //
 // For take sizes where even 16-draw segments leave the lane chains latency
 // bound (the scalar stream's 2^20 draws), the message recurrence is cut at
-// every draw instead: pass 1 walks the skip in 32-draw segments (one thread
+// every draw instead: pass 1 walks the skip in PD_SEG = 16-draw segments (one thread
 // each, jump-started like K1s) and stores every draw's message increment
 // REDC(s) mod p1, p2, the segments' in-CTA exclusive prefix and the CTA
 // totals; pass 2 runs one thread per draw: a warp-wide inclusive scan of the
@@ -343,7 +343,7 @@ k_pd_draws(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t blocks, 
             draw_tail<E, GF>(P, L, h, c2);
             const uint64_t c = (uint64_t)h * P.p2 + c2;
             if constexpr (RAW) raw[o + (uint64_t)k * mv] = c;
-            if constexpr (F64) f64[o + (uint64_t)k * mv] = to_unit(c, P.n_float, P.n_recip, P.n_recip_lo);
+            if constexpr (F64) f64[o + (uint64_t)k * mv] = to_unit(c, P.n_float, P.n_recip);
             if (d0 + k == blocks - 1) {  // the lane's final state
                 m1[lane] = lane_m1(P, L);
                 m2[lane] = lane_m2(P, L);
@@ -393,7 +393,7 @@ k_scalar_lookahead(const rsa_instance* __restrict__ inst, uint64_t m1_0, uint64_
             draw_tail<E, GF>(P, Ln, h, c2);
             const uint64_t c = (uint64_t)h * P.p2 + c2;
             raw[k0 + k] = c;
-            f64[k0 + k] = to_unit(c, P.n_float, P.n_recip, P.n_recip_lo);
+            f64[k0 + k] = to_unit(c, P.n_float, P.n_recip);
             tm1[k0 + k] = (uint32_t)lane_m1(P, Ln);
             tm2[k0 + k] = (uint32_t)lane_m2(P, Ln);
         }

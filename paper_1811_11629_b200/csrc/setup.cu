@@ -89,8 +89,7 @@ RSA_DEV void build_instance(rsa_instance* o, uint32_t p1, uint32_t p2, uint32_t 
     v.b = n >= (1ull << 32) ? mulmod64_fp(qm, hm, n) : mulmod64(qm, hm, n);
     v.n_float = __ull2double_rn(n);
     v.n_recip = __drcp_rn(v.n_float);
-    v.n_recip_lo = __dmul_rn(__fma_rn(-v.n_float, v.n_recip, 1.0), v.n_recip);
-    v.skip_const = 0; v.reserved2 = 0;
+    v.skip_const = 0; v.reserved1 = 0; v.reserved2 = 0;
     *o = v;
 }
 

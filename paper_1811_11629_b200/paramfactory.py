@@ -342,7 +342,7 @@ def derive_stream_params(key: StreamKey, e: int = rsacore.DEFAULT_EXPONENT,
     ordinal, a_index = stream_indices(key, n_a)
     skip = SkipParams.create(multiplier_table[a_index] if multiplier is None else multiplier)
     exhausted = DerivationExhausted(f"no valid parameters within {MAX_STEPS} ordinals of {ordinal}")
-    if min(key.stream_id, key.master_seed) < 0 or not _exponent_usable(e):
+    if not _exponent_usable(e):  # negative keys reduce mod S like the reference's (paramfactory.py:249)
         raise exhausted
     step = 0
     while step < MAX_STEPS:

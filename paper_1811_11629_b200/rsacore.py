@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import functools
 import math
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -176,17 +177,8 @@ def _instance_record(params: GeneratorParams) -> np.ndarray:
     r["n"], r["q"], r["b"] = params.n, sk.q, params.b
     r["n_float"] = float(params.n)
     r["n_recip"] = 1.0 / float(params.n)
-    r["n_recip_lo"] = recip_lo(r["n_float"], r["n_recip"])
     r["skip_const"] = params.skip_const
     return rec
-
-
-def recip_lo(nf: float, y: float) -> float:
-    """RN(RN(1 - nf*y) * y) with the inner residual exact (as the device's
-    fma(-nf, y, 1) computes it): the low half of 1/nf ~ y + y_lo."""
-    from fractions import Fraction
-    e = float(1 - Fraction(nf) * Fraction(y))       # exactly representable
-    return float(Fraction(e) * Fraction(y))          # single rounding
 
 
 @functools.lru_cache(maxsize=256)
@@ -283,13 +275,30 @@ class _Lookahead:
     __slots__ = ("params", "raw", "f64", "s", "m1", "m2", "pos", "expect")
 
 
+# Look-ahead buffers live beside the states, keyed by id(state) and dropped
+# when the state is collected: vars(state) stays the reference's four fields,
+# and copy / deepcopy / pickle of a state carry no buffer (a copy refills).
+_LOOKAHEADS: dict[int, _Lookahead] = {}
+
+
+def _lookahead_of(state: GeneratorState):
+    return _LOOKAHEADS.get(id(state))
+
+
+def _attach_lookahead(state: GeneratorState, lk: _Lookahead) -> None:
+    key = id(state)
+    if key not in _LOOKAHEADS:
+        weakref.finalize(state, _LOOKAHEADS.pop, key, None)
+    _LOOKAHEADS[key] = lk
+
+
 def _lookahead_draw(state: GeneratorState, params: GeneratorParams, peek: bool = False):
     """Serve the next draw from the state's look-ahead buffer (refilling it if
     it does not continue this state); None when the instance has no fast
     kernel.  peek=True only answers whether the buffer can serve."""
     if peek:
         return params.skip_mode == SKIP_LCG and bool(instance_flags(params) & _lib.RSA_FLAG_FAST)
-    lk = state.__dict__.get("_lookahead")
+    lk = _lookahead_of(state)
     if (lk is None or lk.pos >= LOOKAHEAD or (lk.params is not params and lk.params != params)
             or lk.expect != (state.m1, state.m2, state.s, state.draws)):
         if params.skip_mode != SKIP_LCG or not instance_flags(params) & _lib.RSA_FLAG_FAST:
@@ -309,7 +318,7 @@ def _lookahead_draw(state: GeneratorState, params: GeneratorParams, peek: bool =
         lk.m1 = host[24 * n:28 * n].view(np.uint32).tolist()
         lk.m2 = host[28 * n:32 * n].view(np.uint32).tolist()
         lk.pos = 0
-        state.__dict__["_lookahead"] = lk
+        _attach_lookahead(state, lk)
     i = lk.pos
     lk.pos = i + 1
     state.m1, state.m2, state.s = lk.m1[i], lk.m2[i], lk.s[i]

@@ -11,6 +11,8 @@ chunk computes.
 
 from __future__ import annotations
 
+import os
+import threading
 from collections import OrderedDict
 from dataclasses import dataclass, field
 
@@ -126,47 +128,62 @@ def _fill(state: VectorState, blocks: int, raw: torch.Tensor | None, f64: torch.
 _GRAPHS: "OrderedDict[tuple, tuple]" = OrderedDict()
 _SEEN: "OrderedDict[tuple, None]" = OrderedDict()
 _GRAPH_MAX = 8
+_GRAPH_LOCK = threading.Lock()
+# RSARAND_GRAPH_REPLAY=0 turns the replay off (every call launches directly)
+_GRAPH_REPLAY = os.environ.get("RSARAND_GRAPH_REPLAY", "1") != "0"
 
 
 def clear_graph_cache() -> None:
     """Drop the captured segmented-fill graphs (and the scratch they hold)."""
-    _GRAPHS.clear()
-    _SEEN.clear()
+    with _GRAPH_LOCK:
+        _GRAPHS.clear()
+        _SEEN.clear()
 
 
 def _segmented_launch(key: tuple, launch, keep: torch.Tensor) -> None:
     d = keep.device
-    hit = _GRAPHS.get(key)
-    if hit is not None:
-        _GRAPHS.move_to_end(key)
-        if torch.cuda.current_device() == d.index:
-            hit[0].replay()
-        else:
-            with torch.cuda.device(d):
-                hit[0].replay()
-        return
-    if key not in _SEEN:
-        _SEEN[key] = None
-        if len(_SEEN) > 4 * _GRAPH_MAX:
-            _SEEN.popitem(last=False)
+    # inside a caller's own capture the launches simply join that graph
+    if not _GRAPH_REPLAY or torch.cuda.is_current_stream_capturing():
         launch()
         return
+    with _GRAPH_LOCK:
+        hit = _GRAPHS.get(key)
+        if hit is not None:
+            _GRAPHS.move_to_end(key)
+            action = "replay"
+        elif key not in _SEEN:
+            _SEEN[key] = None
+            if len(_SEEN) > 4 * _GRAPH_MAX:
+                _SEEN.popitem(last=False)
+            action = "direct"
+        else:
+            del _SEEN[key]  # second identical call: capture it
+            action = "capture"
+    if action == "direct":
+        launch()
+        return
+    if action == "replay":
+        with torch.cuda.device(d):
+            hit[0].replay()
+        return
     # capture on a side stream without torch.cuda.graph's synchronize /
-    # gc / empty_cache (only our own kernels are recorded)
+    # gc / empty_cache (only our own kernels are recorded); thread-local
+    # capture mode, so other threads' CUDA calls (allocator) stay legal
     cur = torch.cuda.current_stream(d)
     side = torch.cuda.Stream(device=d)
     side.wait_stream(cur)
     g = torch.cuda.CUDAGraph()
     with torch.cuda.device(d), torch.cuda.stream(side):
-        g.capture_begin()
+        g.capture_begin(capture_error_mode="thread_local")
         try:
             scratch = launch()
         finally:
             g.capture_end()
     cur.wait_stream(side)
-    _GRAPHS[key] = (g, keep, scratch)
-    if len(_GRAPHS) > _GRAPH_MAX:
-        _GRAPHS.popitem(last=False)
+    with _GRAPH_LOCK:
+        _GRAPHS[key] = (g, keep, scratch)
+        if len(_GRAPHS) > _GRAPH_MAX:
+            _GRAPHS.popitem(last=False)
     with torch.cuda.device(d):
         g.replay()
 

@@ -221,8 +221,8 @@ def test_clamp_and_float_map(p0, golden_vectors):
 
 
 def test_lane_seeds(p0, golden_vectors):
-    assert np.array_equal(u64np(skipgen.lane_offset_seeds(p0.skip, 1, 64)), golden_vectors["lane_seeds_mv64"])
-    assert np.array_equal(u64np(skipgen.lane_offset_seeds(p0.skip, 777, 64)),
+    assert np.array_equal(np.array(skipgen.lane_offset_seeds(p0.skip, 1, 64), dtype=np.uint64), golden_vectors["lane_seeds_mv64"])
+    assert np.array_equal(np.array(skipgen.lane_offset_seeds(p0.skip, 777, 64), dtype=np.uint64),
                           golden_vectors["lane_seeds_mv64_s0_777"])
     v = R.init_vector(p0, mv=64)
     assert np.array_equal(u64np(v.s), golden_vectors["lane_seeds_mv64"])
@@ -448,12 +448,25 @@ def test_vector_snapshot_restore_and_jump(p0):
 def test_vector_equals_interleaved_scalar_streams(p0, mv):
     """Reference acceptance c09 (test_acceptance.py:192-206): take_floats at Mv
     equals the block-major interleave of Mv scalar streams seeded with the lane
-    offsets, 10^5 blocks, bit-exact."""
+    offsets, 10^5 blocks, bit-exact.  The scalar side is independent of this
+    package: lane seeds from the oracle's skip_power restatement
+    (skipgen.py:124-138), every lane's scalar stream from the C oracle, and up
+    to 4 lanes also from the pure-Python-int scalar recurrence
+    (oracle.scalar_raws, rsacore.py:236-258) mapped by floats_from_raw."""
+    from oracle import coracle
     blocks = 100_000
-    got = u64np(R.take_floats(R.init_vector(p0, mv=mv), blocks * mv))
-    seeds = [int(x) for x in u64np(skipgen.lane_offset_seeds(p0.skip, 1, mv))]
-    lanes = [np.asarray(rsacore.take_floats(rsacore.init(p0, 0, s0), p0, blocks)) for s0 in seeds]
-    assert np.array_equal(got, np.array(lanes).T.reshape(-1))
+    got = R.take_floats(R.init_vector(p0, mv=mv), blocks * mv).cpu().numpy().reshape(blocks, mv)
+    P = O.Params(p0.p1, p0.p2, p0.e, p0.skip.a)
+    seeds = O.lane_seeds(P, 1, mv)
+    assert skipgen.lane_offset_seeds(p0.skip, 1, mv) == [int(x) for x in seeds]
+    z = np.zeros(1, dtype=np.uint64)
+    for g in range(mv):
+        _, f = coracle.fill(coracle.params(P.p1, P.p2, P.e, P.a), z.copy(), z.copy(), seeds[g:g + 1].copy(),
+                            blocks, raw=False)
+        assert np.array_equal(got[:, g], f.reshape(-1)), f"lane {g} differs from the C-oracle scalar stream"
+    for g in sorted({0, mv // 3, (2 * mv) // 3, mv - 1}):
+        raws = np.array(O.scalar_raws(P, blocks, m0=0, s0=int(seeds[g])), dtype=np.uint64)
+        assert np.array_equal(got[:, g], O.floats_from_raw(raws, P)), f"lane {g} vs Python-int scalar stream"
 
 
 @pytest.mark.parametrize("mv,blocks,stride_pad", [(1, 20000, 0), (5, 4000, 3), (64, 9000, 16), (64, 40000, 2)])
@@ -594,6 +607,49 @@ def test_repeated_takes_replay_graph_equal_stream(p0, mv, n):
     assert st.draws == ref.draws
     vecgen.clear_graph_cache()
     assert not vecgen._GRAPHS
+
+
+def test_segmented_take_inside_user_capture(p0):
+    """A repeated identical segmented take inside the caller's own CUDA-graph
+    capture joins that graph instead of nesting a capture."""
+    vecgen.clear_graph_cache()
+    st = R.init_vector(p0, m0=9, mv=64)
+    out = torch.empty(64 * 4096, dtype=torch.float64, device="cuda")
+    R.take_floats(st, out.numel(), out=out)  # first call: direct launch
+    ref = R.init_vector(p0, m0=9, mv=64)
+    want = u64np(R.take_floats(ref, 3 * out.numel()))
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        g.capture_begin()
+        R.take_floats(st, out.numel(), out=out)  # the second identical call, under capture
+        g.capture_end()
+    torch.cuda.current_stream().wait_stream(s)
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(u64np(out), want[out.numel():2 * out.numel()])
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(u64np(out), want[2 * out.numel():])
+    vecgen.clear_graph_cache()
+
+
+def test_lookahead_stays_out_of_state_image(p0):
+    """The scalar look-ahead buffer is kept beside the state: vars(state) is
+    the reference's four fields, and copies / pickles continue the stream."""
+    import copy
+    import pickle
+    st = rsacore.init(p0, m0=31337)
+    rsacore.next_raw(st, p0)
+    assert set(vars(st)) == {"m1", "m2", "s", "draws"}
+    a, b = copy.deepcopy(st), pickle.loads(pickle.dumps(st))
+    want = [rsacore.next_raw(st, p0) for _ in range(5)]
+    assert [rsacore.next_raw(a, p0) for _ in range(5)] == want
+    assert [rsacore.next_raw(b, p0) for _ in range(5)] == want
+    n = len(rsacore._LOOKAHEADS)
+    del a, b
+    assert len(rsacore._LOOKAHEADS) == n - 2
 
 
 def test_scalar_lookahead_matches_reference_steps(p0):

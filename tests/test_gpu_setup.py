@@ -154,6 +154,18 @@ def test_derive_stream_params_matches_reference(golden_streams):
         R.derive_stream_params(R.StreamKey(1, 2), e=4)
 
 
+def test_derive_negative_keys_like_reference():
+    """Negative stream ids / master seeds reduce mod S exactly as the
+    reference's Python % does (paramfactory.py:249); values computed with the
+    reference in the build container."""
+    want = {(R.DEFAULT_MASTER_SEED, -5): (2669237027, 3455433887, 3003776879),
+            (-12345, 77): (2975481599, 3099791447, 3027930091),
+            (-1, -1): (2229924539, 4136181143, 2966714411)}
+    for (seed, sid), (p1, p2, a) in want.items():
+        p = R.derive_stream_params(R.StreamKey(seed, sid))
+        assert (p.p1, p.p2, p.skip.a) == (p1, p2, a), (seed, sid)
+
+
 def test_derive_all_2e20(golden_derive_all, golden_streams):
     """Config 5: 2^20 instance tuples built on the device, packed like the
     golden digest (computed by the reference), plus device-only constants
