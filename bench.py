@@ -485,7 +485,7 @@ def run_gpu(args):
                     "dtype": "u32 Montgomery / u64 skip + f64 map", "data": "synthetic: derived stream params"}
         if main_cfg == 2 and not args.no_sub:
             line["configs"] = {}
-            for c in SUB_CONFIGS:
+            for c in [int(x) for x in args.sub.split(",") if x]:
                 torch.cuda.empty_cache()
                 sub, tables[c] = RUNNERS[c](args, world, rank, local, dev, peak)
                 line["configs"][str(c)] = sub
@@ -513,6 +513,8 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sub", action="store_true", help="config 2 only (no configs{} sub-results)")
+    ap.add_argument("--sub", default=",".join(map(str, SUB_CONFIGS)),
+                    help="comma-separated sub-configurations measured beside config 2 (default: all)")
     ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args(argv)
     if args.gpus < 1:

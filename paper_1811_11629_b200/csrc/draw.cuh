@@ -17,7 +17,7 @@ namespace rsa {
 struct FastInst {
     uint32_t p1, p2, p1_inv, p2_inv, a, k1, k2, garner, r2_1, r2_2, e;
     uint32_t gA, gB;  // fused-Garner constants (draw_fast_hc<E, true>)
-    double n_float, n_recip;
+    double n_float, n_recip, n_recip_lo;  // n_recip_lo: recip_lo(n_float, n_recip), per thread
 };
 
 // Fused Garner (p1's k-correction folded into the Garner product): valid when
@@ -54,6 +54,7 @@ RSA_DEV FastInst load_fast(const rsa_instance* __restrict__ ip) {
     P.gB = P.p1 - P.garner;                            // -p2inv * R mod p1 (garner != 0)
     P.n_float = __ldg(&ip->n_float);
     P.n_recip = __ldg(&ip->n_recip);
+    P.n_recip_lo = recip_lo(P.n_float, P.n_recip);
     return P;
 }
 
@@ -76,10 +77,21 @@ RSA_DEV Lane lane_in(const FastInst& P, uint64_t m1, uint64_t m2, uint64_t s) {
 RSA_DEV uint64_t lane_m1(const FastInst& P, const Lane& L) { return mont_mul(L.x1, P.r2_1, P.p1, P.p1_inv); }
 RSA_DEV uint64_t lane_m2(const FastInst& P, const Lane& L) { return mont_mul(L.x2, P.r2_2, P.p2, P.p2_inv); }
 
-// x + REDC(s) mod p (the message step in the R^-1 domain, vecgen.py:94-95).
-// (Measured alternatives: tools/variants/draw_variants.cuh.)
+// x + REDC(s) mod p (the message step in the R^-1 domain, vecgen.py:94-95),
+// written as x - w with w = (u - s_hi) mod p = -REDC(s) mod p (u = hi(m p),
+// m = s_lo p^-1 mod 2^32; s_hi = s >> 32 < 2^31 < p on the fast path): two
+// modular subtractions, each ISETP + SEL + IADD3 on the ALU, where
+// add_mod(x, REDC(s)) cost a negation and an add that ptxas placed on the
+// IMAD pipe (profiles/r02_ab_draw.txt: +2-5 % per exponent).  Rejected
+// alternatives: tools/variants/draw_variants.cuh.
 RSA_DEV uint32_t msg_add(uint32_t x, uint64_t s, uint32_t p, uint32_t pinv) {
-    return add_mod(x, mont_redc(s, p, pinv), p);
+    const uint32_t m = (uint32_t)s * pinv;
+    const uint32_t u = __umulhi(m, p);
+    const uint32_t vh = (uint32_t)(s >> 32);
+    uint32_t w = u - vh;
+    w = u < vh ? w + p : w;
+    const uint32_t r = x - w;
+    return x < w ? r + p : r;
 }
 
 template <uint32_t E>
@@ -112,7 +124,9 @@ RSA_DEV void draw_tail(const FastInst& P, const Lane& L, uint32_t& h, uint32_t& 
     uint32_t y1 = pow_e<E>(L.x1, P.e, P.p1, P.p1_inv);   // m1^e R^-(2e-1)
     uint32_t y2 = pow_e<E>(L.x2, P.e, P.p2, P.p2_inv);
     c2 = mont_mul(y2, P.k2, P.p2, P.p2_inv);             // m2^e mod p2
-    uint32_t c2r = c2 >= P.p1 ? c2 - P.p1 : c2;          // c2 < 2^32 < 2 p1
+    // c2 < 2^32 < 2 p1: the conditional subtract as an unsigned min (one
+    // VIADDMNMX on the ALU; c2 - p1 wraps above c2 exactly when c2 < p1)
+    uint32_t c2r = min(c2, c2 - P.p1);
     if constexpr (GF) {
         uint64_t t = (uint64_t)y1 * P.gA + (uint64_t)c2r * P.gB;  // < 2 p1^2 < 2^64
         uint32_t m = (uint32_t)t * P.p1_inv;
@@ -120,7 +134,7 @@ RSA_DEV void draw_tail(const FastInst& P, const Lane& L, uint32_t& h, uint32_t& 
         uint32_t th = (uint32_t)(t >> 32);
         uint32_t r = th - u;
         r = th < u ? r + P.p1 : r;
-        h = r >= P.p1 ? r - P.p1 : r;
+        h = min(r, r - P.p1);  // r < 2 p1, as for c2r
     } else {
         uint32_t c1 = mont_mul(y1, P.k1, P.p1, P.p1_inv);  // m1^e mod p1
         uint32_t d = sub_mod(c1, c2r, P.p1);
@@ -135,10 +149,11 @@ RSA_DEV uint64_t draw_fast(const FastInst& P, Lane& L) {
     return (uint64_t)h * P.p2 + c2;
 }
 
-// One draw mapped to r = min(fl(c)/fl(n), 1-2^-53) (vecgen.py:103-107).
+// One draw mapped to r = min(fl(c)/fl(n), 1-2^-53) (vecgen.py:103-107), the
+// 4-op quotient (fused consumer).
 template <uint32_t E, bool GF>
 RSA_DEV double draw_unit(const FastInst& P, Lane& L) {
-    return to_unit(draw_fast<E, GF>(P, L), P.n_float, P.n_recip);
+    return to_unit_dd(draw_fast<E, GF>(P, L), P.n_float, P.n_recip, P.n_recip_lo);
 }
 
 // ---- general path (test-mode sizes, any prime q, unit/const skip) -------------

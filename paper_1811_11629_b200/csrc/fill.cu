@@ -65,8 +65,13 @@ k_fill_fast(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t total_l
         off = (uint64_t)g * ilv + i;
         step = (uint64_t)mv * ilv;
     }
+    // per-exponent schedule choices measured on B200 (profiles/r02_ab_draw.txt):
+    // the 4-op quotient at e = 3, a 2x-unrolled block loop at e = 5 and 9
+    constexpr bool DD = E == 3;
+    constexpr int UNROLL = (E == 5 || E == 9) ? 2 : 1;
     with_garner(P, [&](auto gf) {
         constexpr bool GF = decltype(gf)::value;
+#pragma unroll UNROLL
         for (uint64_t k = 0; k < blocks; ++k, off += step) {
             uint64_t c[LPT];
 #pragma unroll
@@ -76,7 +81,8 @@ k_fill_fast(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t total_l
                 double r[LPT];
 #pragma unroll
                 for (int j = 0; j < LPT; ++j)
-                    r[j] = F64 == 1 ? to_unit(c[j], P.n_float, P.n_recip)
+                    r[j] = F64 == 1 ? (DD ? to_unit_dd(c[j], P.n_float, P.n_recip, P.n_recip_lo)
+                                          : to_unit(c[j], P.n_float, P.n_recip))
                                     : __uint2double_rn((uint32_t)c[j]) * 0x1p-32;
                 store_f64<LPT>(f64 + off, r);
             }

@@ -211,6 +211,20 @@ RSA_DEV double div_rn(double x, double N, double y) {
     return __fma_rn(r, y, q);
 }
 
+// The same quotient in 4 FP64 ops from the double-double reciprocal y + y_lo,
+// y_lo = RN((1 - N y) y) (1 - N y is exact for y = RN(1/N)): x (y + y_lo) is
+// within ~2^-104 relative of x/N, so q0 = RN(x y + RN(x y_lo)) is faithful
+// and one Markstein step rounds it correctly.  Faster where the FP64 slot is
+// worth more than the extra register (fused consumer, e = 3 fill: +1.0-1.3 %,
+// profiles/r02_ab_draw.txt); slower at e = 65537, which keeps div_rn.
+RSA_DEV double div_rn_dd(double x, double N, double y, double y_lo) {
+    double q = __fma_rn(x, y, __dmul_rn(x, y_lo));
+    double r = __fma_rn(-q, N, x);
+    return __fma_rn(r, y, q);
+}
+
+RSA_DEV double recip_lo(double N, double y) { return __dmul_rn(__fma_rn(-N, y, 1.0), y); }
+
 // r = min(fl(c)/fl(n), MAX_BELOW_ONE)  (vecgen.py:103-107)
 RSA_DEV double unit_from_fl(double x, double n_float, double n_recip) {
     double r = div_rn(x, n_float, n_recip);
@@ -219,6 +233,11 @@ RSA_DEV double unit_from_fl(double x, double n_float, double n_recip) {
 
 RSA_DEV double to_unit(uint64_t c, double n_float, double n_recip) {
     return unit_from_fl(__ull2double_rn(c), n_float, n_recip);
+}
+
+RSA_DEV double to_unit_dd(uint64_t c, double n_float, double n_recip, double n_recip_lo) {
+    const double r = div_rn_dd(__ull2double_rn(c), n_float, n_recip, n_recip_lo);
+    return r < 1.0 ? r : MAX_BELOW_ONE;
 }
 
 // ---- primality (setup kernels) --------------------------------------------------
