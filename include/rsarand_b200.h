@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define RSA_ABI_VERSION 3
+#define RSA_ABI_VERSION 4
 
 /* status codes */
 #define RSA_OK 0
@@ -283,6 +283,73 @@ int rsa_setup_instances(const rsa_setup_config* cfg, uint64_t count,
 
 int rsa_battery_count(int test, const double* v, uint64_t n, uint32_t p1, uint32_t p2,
                       unsigned long long* counts, int* flag, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Fused battery counting (consumers fed in registers like
+ * K2).  The variates of a BitSource over n_inst interleaved streams
+ * (stats.BitSource, stats.py:118-136: round-robin by draw, stream 0 first —
+ * the RSA_FLAG_INTERLEAVE order) are generated for `blocks` whole blocks of
+ * every stream and counted without ever being written: each CTA holds a tile
+ * of RSA_BT_TILE consecutive positions in shared memory, counts the tuples
+ * that lie inside it, and hands the variates of the (at most one) tuple
+ * straddling each tile boundary to a slot; rsa_battery_stitch counts those.
+ * Selector: RSA_FLAG_LOW32 ? low 32 bits / 2^32 (raw_low_bits) : the float
+ * map (float_leading).  Lane state advances exactly as rsa_fill would.
+ * Requires n_inst | 256 and (mv * n_inst) % RSA_BT_TILE == 0.
+ *
+ * spec->pos0 is the test-relative position of the first generated variate;
+ * tuples start at test positions 0, d, 2d, ...  Tile t (t = 0 .. blocks *
+ * mv * n_inst / RSA_BT_TILE - 1, in stream order) covers test positions
+ * pos0 + t*RSA_BT_TILE ...; boundary b (b = 0 .. tiles) sits at pos0 +
+ * b*RSA_BT_TILE and owns slots[(spec->seg0 + b) * d .. + d): the part of the
+ * straddling tuple before the boundary at [0, phase), after it at [phase, d),
+ * phase = position mod d.  The caller fills the parts of boundaries 0 and
+ * `tiles` that lie outside the launch (materialised head / tail variates).
+ *
+ * RSA_BT_GAPS: runs of (u > 1/2) / (u <= 1/2) (stats.py gaps_test): runs that
+ * start and end inside one tile are counted (counts[min(len, 64) - 1]); every
+ * tile writes records[spec->seg0 + t] for rsa_battery_gaps_stitch.
+ * rsa_battery_gaps_array does the same over a device array of n variates
+ * (tiles of RSA_BT_TILE, the last one short).
+ * --------------------------------------------------------------------------- */
+#define RSA_BT_GAPS 7
+#define RSA_BT_TILE 256
+
+typedef struct rsa_battery_spec {
+    int32_t test;      /* RSA_BT_HIST / SERIAL / POKER / MAX_OF_T / PERMUTATION / GAPS */
+    uint32_t d;        /* variates per tuple: 1 (HIST, GAPS), d, 5, t, t           */
+    uint32_t p1, p2;   /* as rsa_battery_count (bins / axis / t)                   */
+    uint64_t pos0;     /* test-relative position of the first variate              */
+    uint64_t seg0;     /* first boundary slot / gap record of this launch          */
+} rsa_battery_spec;
+
+typedef struct rsa_gap_record {
+    uint32_t head;     /* values before the tile's first internal flip (or len)    */
+    uint32_t tail;     /* values from its last internal flip to the end (or len)   */
+    uint32_t len;      /* values in the tile                                        */
+    uint32_t bits;     /* 1: has an internal flip, 2: first value > 1/2, 4: last   */
+} rsa_gap_record;
+
+int rsa_battery_fused(const rsa_instance* inst, uint32_t n_inst, uint32_t mv, uint64_t blocks,
+                      uint32_t e, uint32_t flags, uint64_t* m1, uint64_t* m2, uint64_t* s,
+                      const rsa_battery_spec* spec, unsigned long long* counts, int* flag,
+                      double* slots, rsa_gap_record* records, void* stream);
+int rsa_battery_gaps_array(const double* v, uint64_t n, const rsa_battery_spec* spec,
+                           unsigned long long* counts, rsa_gap_record* records, void* stream);
+/* Tuples of boundary slots [first, first + n) whose phase (position mod d,
+ * position = pos0 + (b - seg0) * RSA_BT_TILE for slot b) is nonzero. */
+int rsa_battery_stitch(const rsa_battery_spec* spec, const double* slots, uint64_t first, uint64_t n,
+                       unsigned long long* counts, int* flag, void* stream);
+/* Runs that cross tile boundaries, from n_rec records in stream order (the
+ * test's open final run is not counted). */
+int rsa_battery_gaps_stitch(const rsa_gap_record* records, uint64_t n_rec,
+                            unsigned long long* counts, void* stream);
+/* Fourier cells: the real and imaginary parts of n complex coefficients
+ * (interleaved re, im doubles) binned against 63 sorted interior edges:
+ * counts[cell] (real) and counts[64 + cell] (imag), cell = #edges < value
+ * (numpy searchsorted side='left'). */
+int rsa_battery_fourier_bin(const double* coeff, uint64_t n, const double* edges,
+                            unsigned long long* counts, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Roofline probe: a dependency-free stream of Montgomery triples

@@ -29,6 +29,8 @@ RSA_EALIGN = -5
 
 RSA_SKIP_LCG, RSA_SKIP_UNIT, RSA_SKIP_CONST = 0, 1, 2
 RSA_BT_HIST, RSA_BT_SERIAL, RSA_BT_POKER, RSA_BT_MAX_OF_T, RSA_BT_PERMUTATION, RSA_BT_COLLISION = 1, 2, 3, 4, 5, 6
+RSA_BT_GAPS = 7
+RSA_BT_TILE = 256
 RSA_FLAG_FAST, RSA_FLAG_FIXED, RSA_FLAG_GENERAL_PATH, RSA_FLAG_ONE_LANE = 1, 2, 4, 8
 RSA_FLAG_INTERLEAVE, RSA_FLAG_LOW32 = 16, 32
 
@@ -47,6 +49,13 @@ FUSED_STAT_DTYPE = np.dtype([("s1", "<f8"), ("s2", "<f8"), ("lag", "<f8"), ("fir
                              ("last", "<f8"), ("xy", "<f8")])
 
 
+class BatterySpec(ctypes.Structure):
+    _fields_ = [("test", c_i32), ("d", c_u32), ("p1", c_u32), ("p2", c_u32), ("pos0", c_u64), ("seg0", c_u64)]
+
+
+GAP_RECORD_BYTES = 16  # rsa_gap_record: head, tail, len, bits (uint32 each)
+
+
 class SetupConfig(ctypes.Structure):
     _fields_ = [("seed_mod_S", c_u64), ("first_id", c_u64), ("sigma", c_u64),
                 ("k_p1", c_u64), ("k_p2", c_u64), ("q", c_u64), ("tol", c_u64),
@@ -54,7 +63,7 @@ class SetupConfig(ctypes.Structure):
                 ("max_steps", c_u32), ("start_step", c_u32)]
 
 
-ABI_VERSION = 3  # include/rsarand_b200.h RSA_ABI_VERSION
+ABI_VERSION = 4  # include/rsarand_b200.h RSA_ABI_VERSION
 
 # name -> (restype, argtypes); the CPU test checks this list against include/*.h
 PROTOTYPES = {
@@ -83,6 +92,12 @@ PROTOTYPES = {
                                            c_vp, c_vp, c_u64, c_vp, c_vp, c_vp, c_vp]),
     "rsa_probe_imad": (ctypes.c_int, [c_u32, c_u32, c_vp, ctypes.POINTER(ctypes.c_double), c_vp]),
     "rsa_battery_count": (ctypes.c_int, [ctypes.c_int, c_vp, c_u64, c_u32, c_u32, c_vp, c_vp, c_vp]),
+    "rsa_battery_fused": (ctypes.c_int, [c_vp, c_u32, c_u32, c_u64, c_u32, c_u32, c_vp, c_vp, c_vp,
+                                         ctypes.POINTER(BatterySpec), c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "rsa_battery_gaps_array": (ctypes.c_int, [c_vp, c_u64, ctypes.POINTER(BatterySpec), c_vp, c_vp, c_vp]),
+    "rsa_battery_stitch": (ctypes.c_int, [ctypes.POINTER(BatterySpec), c_vp, c_u64, c_u64, c_vp, c_vp, c_vp]),
+    "rsa_battery_gaps_stitch": (ctypes.c_int, [c_vp, c_u64, c_vp, c_vp]),
+    "rsa_battery_fourier_bin": (ctypes.c_int, [c_vp, c_u64, c_vp, c_vp, c_vp]),
     "rsa_abi_version": (ctypes.c_int, []),
     "rsa_built_arch": (ctypes.c_int, []),
     "rsa_last_error": (ctypes.c_char_p, []),

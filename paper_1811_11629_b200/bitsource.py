@@ -92,6 +92,52 @@ class BitSource:
         return parts[0] if len(parts) == 1 else torch.cat(parts)
 
 
+    # ---- fused counting (stats.py: the battery consumers fed in registers) ----
+
+    def fused_target(self) -> tuple | None:
+        """(instance table, m1, m2, s) when whole blocks of this source can be
+        generated and counted in one rsa_battery_fused launch (the selector's
+        variates, same Mv / exponent / fast kernel for every stream, the
+        stream count dividing the CTA, a block a whole number of tiles, and
+        the streams in lockstep); None otherwise."""
+        if self.selector not in ("float_leading", "raw_low_bits"):
+            return None
+        st = self.streams
+        k, mv = len(st), st[0].mv
+        if 256 % k or (mv * k) % _lib.RSA_BT_TILE or len({x._pending.numel() for x in st}) != 1:
+            return None
+        if k == 1:
+            x = st[0]
+            if not instance_flags(x.params) & _lib.RSA_FLAG_FAST:
+                return None
+            return device_instance(x.params, x.device), x.m1, x.m2, x.s
+        return self._fused
+
+    def buffered(self) -> int:
+        """Variates available without generating a new block (the surplus
+        buffer plus every stream's pending draws)."""
+        buf = 0 if self._buffer is None else self._buffer.numel()
+        return buf + len(self.streams) * self.streams[0]._pending.numel()
+
+    def count_fused(self, blocks: int, spec, counts: torch.Tensor, flag: torch.Tensor | None,
+                    slots: torch.Tensor | None, records: torch.Tensor | None) -> None:
+        """Generate `blocks` whole blocks of every stream and count them with
+        rsa_battery_fused (nothing is materialised); the streams advance
+        exactly as take(blocks * Mv * k) would advance them.  Call only when
+        buffered() == 0."""
+        target = self.fused_target()
+        if target is None or self.buffered():
+            raise ValueError("this source cannot be counted by the fused kernel")
+        inst, m1, m2, s = target
+        st = self.streams
+        flags = _lib.RSA_FLAG_FAST | (_lib.RSA_FLAG_LOW32 if self.selector == "raw_low_bits" else 0)
+        ptr = lambda t: None if t is None else t.data_ptr()
+        _lib.call("rsa_battery_fused", inst.data_ptr(), len(st), st[0].mv, blocks, st[0].params.e, flags,
+                  m1.data_ptr(), m2.data_ptr(), s.data_ptr(), spec, counts.data_ptr(), ptr(flag), ptr(slots),
+                  ptr(records), _device.stream(st[0].device))
+        for x in st:
+            x.draws += blocks * x.mv
+
     def _per_stream(self, rounds: int) -> torch.Tensor:
         views = [self._view(vecgen.take_raw(st, rounds), st) for st in self.streams]
         return torch.stack(views).T.reshape(-1)

@@ -24,7 +24,7 @@ def test_library_builds_and_loads():
     path = _build.build()
     assert os.path.exists(path)
     lib = _lib.load()
-    assert lib.rsa_abi_version() == _lib.ABI_VERSION == 3
+    assert lib.rsa_abi_version() == _lib.ABI_VERSION == 4
     assert lib.rsa_built_arch() == 100
 
 
@@ -65,6 +65,22 @@ def test_struct_layouts_match(tmp_path):
     assert sizes == [128, ctypes.sizeof(_lib.SetupConfig), _lib.FUSED_STAT_DTYPE.itemsize]
     assert offs[:len(fields)] == [_lib.INSTANCE_DTYPE.fields[f][1] for f in fields]
     assert offs[len(fields):] == [getattr(_lib.SetupConfig, f).offset for f in cfg_fields]
+
+
+def test_battery_struct_layouts_match(tmp_path):
+    spec_fields = [f for f, _ in _lib.BatterySpec._fields_]
+    src = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void){"]
+    src.append('printf("%zu %zu %d %d\\n", sizeof(rsa_battery_spec), sizeof(rsa_gap_record), RSA_BT_TILE, RSA_BT_GAPS);')
+    for f in spec_fields:
+        src.append(f'printf("%zu\\n", offsetof(rsa_battery_spec, {f}));')
+    src.append("return 0;}")
+    c = tmp_path / "bt.c"
+    c.write_text("\n".join(src))
+    exe = tmp_path / "bt"
+    subprocess.run(["gcc", "-std=c11", "-o", str(exe), str(c)], check=True)
+    vals = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()))
+    assert vals[:4] == [ctypes.sizeof(_lib.BatterySpec), _lib.GAP_RECORD_BYTES, _lib.RSA_BT_TILE, _lib.RSA_BT_GAPS]
+    assert vals[4:] == [getattr(_lib.BatterySpec, f).offset for f in spec_fields]
 
 
 def test_argument_errors_need_no_gpu():
