@@ -350,6 +350,14 @@ int rsa_battery_gaps_stitch(const rsa_gap_record* records, uint64_t n_rec,
  * (numpy searchsorted side='left'). */
 int rsa_battery_fourier_bin(const double* coeff, uint64_t n, const double* edges,
                             unsigned long long* counts, void* stream);
+/* *out = sum over i < n of (counts[i] - e)^2, each term and every addition
+ * rounded exactly as numpy's np.square(counts - e).sum() (pairwise summation,
+ * blocks of 128 with eight accumulators): the equiprobable tests' statistic
+ * without moving the count vector to the host.  Scratch: device memory of
+ * rsa_battery_chi2_scratch_bytes(n) bytes (0 when n is out of range). */
+uint64_t rsa_battery_chi2_scratch_bytes(uint64_t n);
+int rsa_battery_chi2_sum(const long long* counts, uint64_t n, double e, double* out, void* scratch,
+                         uint64_t scratch_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Roofline probe: a dependency-free stream of Montgomery triples

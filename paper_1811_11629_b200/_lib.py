@@ -98,6 +98,8 @@ PROTOTYPES = {
     "rsa_battery_stitch": (ctypes.c_int, [ctypes.POINTER(BatterySpec), c_vp, c_u64, c_u64, c_vp, c_vp, c_vp]),
     "rsa_battery_gaps_stitch": (ctypes.c_int, [c_vp, c_u64, c_vp, c_vp]),
     "rsa_battery_fourier_bin": (ctypes.c_int, [c_vp, c_u64, c_vp, c_vp, c_vp]),
+    "rsa_battery_chi2_scratch_bytes": (c_u64, [c_u64]),
+    "rsa_battery_chi2_sum": (ctypes.c_int, [c_vp, c_u64, ctypes.c_double, c_vp, c_vp, c_u64, c_vp]),
     "rsa_abi_version": (ctypes.c_int, []),
     "rsa_built_arch": (ctypes.c_int, []),
     "rsa_last_error": (ctypes.c_char_p, []),

@@ -466,3 +466,147 @@ extern "C" int rsa_battery_fourier_bin(const double* coeff, uint64_t n, const do
     k_bat_fourier_bin<<<grid, 256, 0, as_stream(stream)>>>(coeff, n, edges, counts);
     return launch_status("rsa_battery_fourier_bin");
 }
+
+// ---- chi-square sum in numpy's order -------------------------------------------
+//
+// The equiprobable tests' statistic is float(np.square(counts - e).sum() / e)
+// (stats.py: _uniform_report).  numpy sums a contiguous float64 vector
+// pairwise (numpy/_core/src/umath/loops_utils.h.src, pairwise_sum): n < 8
+// sequentially from 0.0; n <= 128 with eight strided accumulators combined
+// as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a sequential remainder;
+// otherwise split at n2 = n/2 rounded down to a multiple of 8 and add the two
+// halves.  Restated here exactly (tree built level by level, leaves in
+// parallel, internal nodes bottom-up), so the device statistic is
+// bit-identical to the host's and only one double leaves the GPU.
+
+struct PwNode {
+    uint64_t off;
+    uint32_t size;
+    uint32_t child;  // first child's node index; PW_LEAF for leaves
+};
+constexpr uint32_t PW_LEAF = 0xFFFFFFFFu;
+constexpr int PW_MAX_LEVELS = 62;
+
+__device__ __forceinline__ double pw_term(const long long* c, uint64_t i, double e) {
+    const double d = __dsub_rn(__ll2double_rn(c[i]), e);
+    return __dmul_rn(d, d);
+}
+
+__device__ double pw_leaf(const long long* c, uint32_t n, double e) {
+    if (n < 8) {
+        double r = 0.0;
+        for (uint32_t i = 0; i < n; ++i) r = __dadd_rn(r, pw_term(c, i, e));
+        return r;
+    }
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = pw_term(c, j, e);
+    uint32_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], pw_term(c, i + j, e));
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, pw_term(c, i, e));
+    return res;
+}
+
+// One CTA: the recursion tree level by level.  levels[0] = number of levels,
+// levels[1 + L] = first node index of level L (levels[1 + nlev] = node count).
+__global__ void __launch_bounds__(1024) k_pw_build(uint64_t n, PwNode* __restrict__ nodes, uint32_t* __restrict__ levels) {
+    __shared__ uint32_t base[PW_MAX_LEVELS + 2];
+    __shared__ uint32_t scan[1024];
+    const uint32_t t = threadIdx.x;
+    if (t == 0) {
+        nodes[0].off = 0;
+        nodes[0].size = (uint32_t)n;
+        base[0] = 0;
+        base[1] = 1;
+    }
+    int L = 0;
+    for (;; ++L) {
+        __syncthreads();
+        const uint32_t b0 = base[L], b1 = base[L + 1];
+        if (b1 == b0 || L >= PW_MAX_LEVELS) break;
+        const uint32_t cnt = b1 - b0, per = (cnt + 1023) / 1024;
+        const uint32_t lo = b0 + t * per < b1 ? b0 + t * per : b1;
+        const uint32_t hi = lo + per < b1 ? lo + per : b1;
+        uint32_t mine = 0;
+        for (uint32_t i = lo; i < hi; ++i) mine += nodes[i].size > 128;
+        scan[t] = mine;
+        __syncthreads();
+        for (uint32_t w = 1; w < 1024; w <<= 1) {  // inclusive Hillis-Steele scan
+            const uint32_t v = t >= w ? scan[t - w] : 0;
+            __syncthreads();
+            scan[t] += v;
+            __syncthreads();
+        }
+        uint32_t next = b1 + 2 * (scan[t] - mine);
+        for (uint32_t i = lo; i < hi; ++i) {
+            const uint32_t sz = nodes[i].size;
+            if (sz > 128) {
+                uint32_t n2 = sz / 2;
+                n2 -= n2 % 8;
+                nodes[i].child = next;
+                nodes[next].off = nodes[i].off;
+                nodes[next].size = n2;
+                nodes[next + 1].off = nodes[i].off + n2;
+                nodes[next + 1].size = sz - n2;
+                next += 2;
+            } else {
+                nodes[i].child = PW_LEAF;
+            }
+        }
+        if (t == 1023) base[L + 2] = b1 + 2 * scan[1023];
+    }
+    __syncthreads();
+    if (t == 0) levels[0] = (uint32_t)L;
+    for (int l = t; l <= L; l += 1024) levels[1 + l] = base[l];
+}
+
+__global__ void k_pw_leaves(const long long* __restrict__ c, double e, const PwNode* __restrict__ nodes,
+                            const uint32_t* __restrict__ levels, double* __restrict__ vals) {
+    const uint32_t total = levels[1 + levels[0]];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const PwNode nd = nodes[i];
+        if (nd.child == PW_LEAF) vals[i] = pw_leaf(c + nd.off, nd.size, e);
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_pw_combine(const PwNode* __restrict__ nodes, const uint32_t* __restrict__ levels,
+                                                     double* __restrict__ vals, double* __restrict__ out) {
+    const int nlev = (int)levels[0];
+    for (int L = nlev - 1; L >= 0; --L) {
+        const uint32_t b0 = levels[1 + L], b1 = levels[2 + L];
+        for (uint32_t i = b0 + threadIdx.x; i < b1; i += 1024) {
+            const uint32_t ch = nodes[i].child;
+            if (ch != PW_LEAF) vals[i] = __dadd_rn(vals[ch], vals[ch + 1]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = vals[0];
+}
+
+extern "C" uint64_t rsa_battery_chi2_scratch_bytes(uint64_t n) {
+    if (n == 0 || n > 0xFFFFFFFFull) return 0;
+    const uint64_t nodes = 4 * (n / 64 + 1) + 64;  // leaves hold >= 64 values except a root below 128
+    return nodes * (sizeof(PwNode) + sizeof(double)) + (PW_MAX_LEVELS + 2) * sizeof(uint32_t) + 64;
+}
+
+extern "C" int rsa_battery_chi2_sum(const long long* counts, uint64_t n, double e, double* out, void* scratch,
+                                    uint64_t scratch_bytes, void* stream) {
+    if (!counts || !out || !scratch || n == 0 || n > 0xFFFFFFFFull) return RSA_EINVAL;
+    if (scratch_bytes < rsa_battery_chi2_scratch_bytes(n)) return RSA_ECAPACITY;
+    const uint64_t max_nodes = 4 * (n / 64 + 1) + 64;
+    char* p = static_cast<char*>(scratch);
+    PwNode* nodes = reinterpret_cast<PwNode*>(p);
+    double* vals = reinterpret_cast<double*>(p + max_nodes * sizeof(PwNode));
+    uint32_t* levels = reinterpret_cast<uint32_t*>(p + max_nodes * (sizeof(PwNode) + sizeof(double)));
+    cudaStream_t st = as_stream(stream);
+    k_pw_build<<<1, 1024, 0, st>>>(n, nodes, levels);
+    unsigned g = grid_for(max_nodes, 256);
+    if (g > 148 * 4) g = 148 * 4;
+    k_pw_leaves<<<g, 256, 0, st>>>(counts, e, nodes, levels, vals);
+    k_pw_combine<<<1, 1024, 0, st>>>(nodes, levels, vals, out);
+    return launch_status("rsa_battery_chi2_sum");
+}

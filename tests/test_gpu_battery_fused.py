@@ -156,3 +156,15 @@ def test_fused_rejects_unsupported_layouts():
     spec = _lib.BatterySpec(test=_lib.RSA_BT_SERIAL, d=2, p1=2, p2=1024, pos0=0, seg0=0)
     assert _lib.load().rsa_battery_fused(None, 3, 256, 1, 9, 1, None, None, None, spec, None, None, None, None,
                                          None) == _lib.RSA_EINVAL
+
+
+@pytest.mark.parametrize("n", [1, 5, 8, 64, 127, 128, 129, 1000, 4095, 362880, 10 ** 6, 1 << 20, 3628800])
+def test_device_chi2_sum_is_numpys(n):
+    """rsa_battery_chi2_sum restates numpy's pairwise summation of
+    np.square(counts - e): bit-identical for every tree shape."""
+    rng = np.random.default_rng(n)
+    counts = rng.poisson(95.4, n).astype(np.int64)
+    e = 1e8 / n
+    want = np.square(counts - e).sum()
+    got = stats._chi2_sum_device(torch.as_tensor(counts, device="cuda"), e)
+    assert got == float(want)
