@@ -134,9 +134,10 @@ def run_reference_arm(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": statistics.median(walls) * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "u64/u32 modular + f64 map", "data": "synthetic (seeded m0, derived params)",
-            "config": {"workload": "config2 bulk fill (CPU port sample)", "exponents": list(EXPONENTS),
-                       "mv": 65536},
+            "dtype": "u32 Montgomery / u64 skip + f64 map",
+            "data": "synthetic: derived stream params (DEFAULT_MASTER_SEED, stream id = rank), "
+                    "seeded uniform m0 in [0, n)",
+            "config": C.config2_desc(args.gpus, C.seeded_m0(C._stream0().n)),
             "cpu_baseline": cb,
             "e2e": {"value": value, "unit": "Gnumbers/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -356,12 +357,7 @@ def run_config2(args, world, rank, local, dev, peak):
             "dtype": "u32 Montgomery / u64 skip + f64 map",
             "data": "synthetic: derived stream params (DEFAULT_MASTER_SEED, stream id = rank), "
                     "seeded uniform m0 in [0, n)",
-            "config": {"workload": "config2 bulk fill: 2^30 f64 per exponent e in {3,5,17,65537}, "
-                                   "Mv=2^22, 256 blocks, one instance per GPU",
-                       "global_numbers_per_step": w.numbers_per_step,
-                       "mv": w.MV, "blocks": w.BLOCKS, "exponents": list(EXPONENTS), "m0": w.m0,
-                       "l2": "outputs 8 GiB per fill (> L2), no flush needed",
-                       "parallelism": f"independent instances x{world}"},
+            "config": C.config2_desc(world, w.m0),
             "roofline": roofline, "clocks": clk,
             "gpu_launches": launches * args.steps if launches is not None else args.steps * len(EXPONENTS),
             "gpu_launches_source": "CUPTI kernel trace of one extra step x K" if launches is not None

@@ -319,34 +319,71 @@ def _stream0():
         return O.from_fields(json.load(fh)["params"])
 
 
+_C2_SEEDS: np.ndarray | None = None
+
+
+def _c2_lane_seeds(n_lanes: int) -> np.ndarray:
+    """Skip seeds of the first n_lanes lanes of config 2's Mv = 2^22 vector
+    (s0 = 1: lane g starts at a^(g * floor((q-1)/Mv)) mod q, skipgen.py:124-138),
+    by one modular product per lane."""
+    global _C2_SEEDS
+    if _C2_SEEDS is None or len(_C2_SEEDS) < n_lanes:
+        P = _stream0()
+        A = pow(P.a, (P.q - 1) // Config2.MV, P.q)
+        out, x = [], 1
+        for _ in range(n_lanes):
+            out.append(x)
+            x = x * A % P.q
+        _C2_SEEDS = np.array(out, dtype=np.uint64)
+    return _C2_SEEDS[:n_lanes]
+
+
+def config2_desc(world: int, m0: int) -> dict:
+    """The `config` object of the config-2 line (both arms)."""
+    return {"workload": "config2 bulk fill: 2^30 f64 per exponent e in {3,5,17,65537}, Mv=2^22, 256 blocks, "
+                        "one instance per GPU",
+            "global_numbers_per_step": world * len(EXPONENTS) * Config2.MV * Config2.BLOCKS,
+            "mv": Config2.MV, "blocks": Config2.BLOCKS, "exponents": list(EXPONENTS), "m0": m0,
+            "l2": "outputs 8 GiB per fill (> L2), no flush needed",
+            "parallelism": f"independent instances x{world}"}
+
+
 def _cpu_cfg2(args):
-    """vecgen's lockstep path (numpy port) at Mv = 65536 for each bench exponent."""
+    """vecgen's lockstep path (numpy port) over lanes [lo, hi) of config 2's
+    Mv = 2^22 vector (stream 0, seeded m0), for each bench exponent."""
     import time
     from oracle import rsa_oracle as O
-    e_list, blocks, mv = args
+    e_list, blocks, lo, hi = args
     P0 = _stream0()
-    st = O.init(P0, m0=seeded_m0(P0.n), mv=mv)
+    m0 = seeded_m0(P0.n)
+    s0 = _c2_lane_seeds(hi)[lo:hi].copy()
     out = {}
     for e in e_list:
         P = dataclasses.replace(P0, e=e)
-        m1, m2, s = st.m1.copy(), st.m2.copy(), st.s.copy()
+        m1 = np.full(hi - lo, m0 % P.p1, dtype=np.uint64)
+        m2 = np.full(hi - lo, m0 % P.p2, dtype=np.uint64)
+        s = s0.copy()
         O.block_raw(m1, m2, s, P)  # warm-up
         t0 = time.perf_counter()
         for _ in range(blocks):
             raw, m1, m2, s = O.block_raw(m1, m2, s, P)
             O.floats_from_raw(raw, P)
-        out[e] = (blocks * mv, time.perf_counter() - t0)
+        out[e] = (blocks * (hi - lo), time.perf_counter() - t0)
     return out
 
 
-def cpu_port_rate(procs: int | None = None, blocks: int = 4, mv: int = 65536) -> dict:
-    """Aggregate numbers/s of the numpy port of vecgen's lockstep path
-    (Mv=65536, the reference CLI bench default, cli.py:26) over all host cores,
-    with the step's exponent mix weighted equally per draw."""
+def cpu_port_rate(procs: int | None = None, blocks: int = 4, lanes_per_proc: int = 65536) -> dict:
+    """Aggregate numbers/s of the numpy port of vecgen's lockstep path on a
+    bounded sample of config 2 itself: each process advances its own
+    contiguous 65536-lane slice (the reference CLI bench's vector width,
+    cli.py:26) of the Mv = 2^22 vector for `blocks` blocks at every bench
+    exponent, all host cores; the step's exponent mix weighted equally per draw."""
     import multiprocessing as mp
     procs = procs or os.cpu_count() or 1
+    _c2_lane_seeds(procs * lanes_per_proc)  # in the parent: the forked workers share it
+    jobs = [(EXPONENTS, blocks, k * lanes_per_proc, (k + 1) * lanes_per_proc) for k in range(procs)]
     with mp.get_context("fork").Pool(procs) as pool:
-        res = pool.map(_cpu_cfg2, [(EXPONENTS, blocks, mv)] * procs)
+        res = pool.map(_cpu_cfg2, jobs)
     per_e = {}
     for e in EXPONENTS:
         draws = sum(r[e][0] for r in res)
@@ -356,9 +393,10 @@ def cpu_port_rate(procs: int | None = None, blocks: int = 4, mv: int = 65536) ->
     draws = sum(r[e][0] for r in res for e in EXPONENTS)
     return {"value": rate / 1e9, "unit": "Gnumbers/s", "cores": procs, "kind": "port",
             "per_e": {str(e): per_e[e] / 1e9 for e in EXPONENTS},
-            "sample": f"numpy port of vecgen lockstep (oracle/rsa_oracle.py), Mv={mv}, {blocks} "
-                      f"blocks per e in {list(EXPONENTS)} per process, {procs} processes "
-                      f"({draws} draws), stream 0 seeded m0; {os.cpu_count()} host cores"}
+            "sample": f"config 2 itself on a bounded sample: lanes [0, {procs * lanes_per_proc}) of the Mv=2^22 "
+                      f"vector (stream 0, seeded m0), {blocks} blocks per e in {list(EXPONENTS)}, one "
+                      f"{lanes_per_proc}-lane slice per process ({procs} processes, {draws} draws); numpy port "
+                      f"of vecgen's lockstep path (oracle/rsa_oracle.py); {os.cpu_count()} host cores"}
 
 
 def _cpu_cfg1(count):
