@@ -243,25 +243,11 @@ def probe_imad_peak(dev) -> dict:
     return {"ops_per_s": best, "sms": sms}
 
 
-def count_launches(fn) -> int | None:
-    """Kernels of this repo's library launched by one call of `fn` (an extra,
-    untimed step), counted from the CUDA activity trace (CUPTI via
-    torch.profiler).  None when the profiler is unavailable."""
-    import torch
-    try:
-        from torch.profiler import ProfilerActivity, profile
-        torch.cuda.synchronize()
-        with profile(activities=[ProfilerActivity.CUDA]) as prof:
-            fn()
-            torch.cuda.synchronize()
-        n = 0
-        for ev in prof.events():
-            name = ev.name or ""
-            if ev.device_type == torch.autograd.DeviceType.CUDA and "rsa::" in name:
-                n += 1
-        return n
-    except Exception:  # pragma: no cover - profiler missing on the box
-        return None
+def launch_count() -> int:
+    """Kernels of this repo's library executed so far in this process (the C
+    ABI's launch counter, corrected for CUDA-graph replays: vecgen.launch_count)."""
+    from paper_1811_11629_b200 import vecgen
+    return vecgen.launch_count()
 
 
 # ---------------------------------------------------------------------------
@@ -283,11 +269,13 @@ def time_workload(w, args, world, local, events_keys=(), min_region_s=0.0):
         ev = {k: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                   for _ in range(args.steps)] for k in events_keys}
     blocks = []
+    launches = None
     barrier_sync(world)
     with ClockSampler(local) as clk:
         while True:
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             barrier_sync(world)
+            c0 = launch_count()
             t0.record(stream)
             for k in range(args.steps):
                 if ev is not None and not blocks:
@@ -295,6 +283,8 @@ def time_workload(w, args, world, local, events_keys=(), min_region_s=0.0):
                 else:
                     w.step()
             t1.record(stream)
+            if launches is None:
+                launches = launch_count() - c0  # this library's kernels in the K timed steps
             barrier_sync(world)
             blocks.append(max_over_ranks(t0.elapsed_time(t1) * 1e-3, world))
             if sum(blocks) >= min_region_s or len(blocks) >= 200:
@@ -302,7 +292,7 @@ def time_workload(w, args, world, local, events_keys=(), min_region_s=0.0):
     per_key = {}
     if ev is not None:
         per_key = {k: statistics.mean(a.elapsed_time(b) * 1e-3 for a, b in ev[k]) for k in events_keys}
-    return statistics.median(blocks), clk.summary(), per_key, len(blocks)
+    return statistics.median(blocks), clk.summary(), per_key, len(blocks), launches
 
 
 # ---------------------------------------------------------------------------
@@ -313,7 +303,7 @@ def run_config2(args, world, rank, local, dev, peak):
     w = C.Config2(dev, world, rank)
     R = w.R
     count = w.count
-    el, clk, per_e, nblocks = time_workload(w, args, world, local, events_keys=EXPONENTS)
+    el, clk, per_e, nblocks, launches = time_workload(w, args, world, local, events_keys=EXPONENTS)
     value = w.numbers_per_step * args.steps / el / 1e9
     dom = max(EXPONENTS, key=lambda e: per_e[e])  # dominant kernel: largest share of the step
     roofline = C.imad_roofline(dom, count, per_e[dom], peak, f"k_fill_fast<{dom}, 2, 0, 1> (e={dom})",
@@ -323,7 +313,6 @@ def run_config2(args, world, rank, local, dev, peak):
                  "imad_frac": w_imad(e) * count / per_e[e] / peak["ops_per_s"],
                  "hbm_frac": roofline["hbm"]["frac"] * per_e[dom] / per_e[e] if roofline["hbm"]["frac"] else None}
         for e in EXPONENTS}
-    launches = count_launches(w.step)
 
     e2e = None
     if not args.no_e2e:
@@ -345,10 +334,25 @@ def run_config2(args, world, rank, local, dev, peak):
                 R.take_floats(st, count, out=host_out)
         barrier_sync(world)
         e2e_t = max_over_ranks(time.perf_counter() - t, world)
+        d2h = len(EXPONENTS) * 8 * count
+        # the bound of this path: a plain pinned device->host copy of 1 GiB, best of 3
+        st = torch.cuda.current_stream()
+        copy_gbs = 0.0
+        for _ in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            host_out[:1 << 27].copy_(w.out[:1 << 27], non_blocking=True)
+            b.record(st)
+            b.synchronize()
+            copy_gbs = max(copy_gbs, 8 * (1 << 27) / (a.elapsed_time(b) * 1e-3) / 1e9)
         e2e = {"value": world * e2e_steps * len(EXPONENTS) * count / e2e_t / 1e9, "unit": "Gnumbers/s",
                "h2d_bytes_per_step": len(EXPONENTS) * 3 * 8 * w.MV,
-               "d2h_bytes_per_step": len(EXPONENTS) * 8 * count,
-               "steps": e2e_steps, "path": "vecgen.take_floats(state, 2^30, out=pinned host)"}
+               "d2h_bytes_per_step": d2h,
+               "steps": e2e_steps, "path": "vecgen.take_floats(state, 2^30, out=pinned host)",
+               "pcie": {"d2h_gbs": d2h * e2e_steps / e2e_t / 1e9, "copy_gbs_measured": copy_gbs,
+                        "frac": d2h * e2e_steps / e2e_t / 1e9 / copy_gbs,
+                        "note": "e2e is bound by the device->host link: 8 B per number leave the GPU; "
+                                "copy_gbs_measured = a plain 1 GiB pinned D2H copy in this run"}}
         del host_out, host_state
 
     line = {"metric": METRIC, "value": value, "unit": "Gnumbers/s", "n_gpus": world,
@@ -359,9 +363,8 @@ def run_config2(args, world, rank, local, dev, peak):
                     "seeded uniform m0 in [0, n)",
             "config": C.config2_desc(world, w.m0),
             "roofline": roofline, "clocks": clk,
-            "gpu_launches": launches * args.steps if launches is not None else args.steps * len(EXPONENTS),
-            "gpu_launches_source": "CUPTI kernel trace of one extra step x K" if launches is not None
-            else "static count (profiler unavailable)",
+            "gpu_launches": launches,
+            "gpu_launches_source": "librsarand_b200 launch counter (rsa_launch_count) over the K timed steps",
             "e2e": e2e, "imad_peak_tops": peak["ops_per_s"] / 1e12,
             "published_context": ("BASELINE.md: the paper's C/OpenMP generator on a 24-core Xeon E5-2680 v3 "
                                   "reached 1.25e8-1.72e8 numbers/s at e <= 17 (PAPER.md:420-421); a different "
@@ -370,21 +373,20 @@ def run_config2(args, world, rank, local, dev, peak):
     return line, None
 
 
-def _sub_line(args, world, value, unit, el, clk, nblocks, config, scaling, launches, static_launches):
+def _sub_line(args, world, value, unit, el, clk, nblocks, config, scaling, launches):
     return {"value": value, "unit": unit, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": el / args.steps * 1e3, "timed_blocks": nblocks, "scaling": scaling,
-            "higher_is_better": True, "config": config, "clocks": clk,
-            "gpu_launches": launches * args.steps if launches is not None else static_launches * args.steps}
+            "higher_is_better": True, "config": config, "clocks": clk, "gpu_launches": launches}
 
 
 def run_config1(args, world, rank, local, dev, peak):
     w = C.Config1(dev, world, rank)
-    el, clk, per_mv, nblocks = time_workload(w, args, world, local, events_keys=w.MVS,
-                                             min_region_s=MIN_REGION_S)
+    el, clk, per_mv, nblocks, launches = time_workload(w, args, world, local, events_keys=w.MVS,
+                                                       min_region_s=MIN_REGION_S)
     line = _sub_line(args, world, w.numbers_per_step * args.steps / el / 1e9, "Gnumbers/s", el, clk, nblocks,
                      {"workload": "config1: stream 0, e=9, 2^20 f64 per take_floats at Mv=1, 64, 65536 "
                                   "(< 2^17 lanes: split across threads by K1p/K1s, graph-replayed)"},
-                     "weak", count_launches(w.step), 6)
+                     "weak", launches)
     line["per_mv"] = {str(mv): {"ms_per_2e20": per_mv[mv] * 1e3, "gnumbers_s": w.COUNT / per_mv[mv] / 1e9}
                       for mv in w.MVS}
     dom = max(w.MVS, key=lambda mv: per_mv[mv])
@@ -399,13 +401,13 @@ def run_config1(args, world, rank, local, dev, peak):
 
 def run_config3(args, world, rank, local, dev, peak):
     w = C.Config3(dev, world, rank)
-    el, clk, _, nblocks = time_workload(w, args, world, local)
+    el, clk, _, nblocks, launches = time_workload(w, args, world, local)
     per = el / args.steps
     line = _sub_line(args, world, w.numbers_per_step * args.steps / el / 1e9, "Gnumbers/s", el, clk, nblocks,
                      {"workload": "config3: 65536 instances (ids 0..65535), e=9, Mv=64, 1024 blocks, "
                                   "2^16 f64 each, instance-major, sharded by contiguous id range",
                       "shard": [w.first, w.n], "l2": "32 GiB output per step (> L2)"},
-                     "strong", count_launches(w.step), 1)
+                     "strong", launches)
     line["roofline"] = C.imad_roofline(9, w.local_numbers, per, peak, "k_fill_fast<9, 2, 0, 1>", "fill_c3",
                                        "fill_e9", clk)
     table = w.table
@@ -415,14 +417,14 @@ def run_config3(args, world, rank, local, dev, peak):
 
 def run_config4(args, world, rank, local, dev, peak):
     w = C.Config4(dev, world, rank)
-    el, clk, _, nblocks = time_workload(w, args, world, local)
+    el, clk, _, nblocks, launches = time_workload(w, args, world, local)
     per = el / args.steps
     line = _sub_line(args, world, w.numbers_per_step * args.steps / el / 1e9, "Gnumbers/s", el, clk, nblocks,
                      {"workload": "config4 fused consumer: 2^20 instances x 2^16 draws, Mv=1, e=9; "
                                   "per-instance mean/var/lag-1/64-bin hist + pooled pair correlation; "
                                   "NCCL all-reduce of pooled stats at N>1", "shard": [w.first, w.n],
                       "l2": "no stream in HBM"},
-                     "strong", count_launches(w.step), 3)
+                     "strong", launches)
     line["roofline"] = C.imad_roofline(9, w.local_numbers, per, peak, "k_fused<9>", "fused", "fused_e9", clk,
                                        hbm_bytes_per_draw=0)
     line["pooled_correlation"] = w.result.pooled_correlation(w.TOTAL // 2)
@@ -439,14 +441,14 @@ def run_config5(args, world, rank, local, dev, peak):
             w.step()
             w.collect()
 
-    el, clk, _, nblocks = time_workload(Timed(), args, world, local, min_region_s=MIN_REGION_S)
+    el, clk, _, nblocks, launches = time_workload(Timed(), args, world, local, min_region_s=MIN_REGION_S)
     line = _sub_line(args, world, w.numbers_per_step * args.steps / el / 1e9, "Gcandidates/s", el, clk, nblocks,
                      {"workload": "config5 setup: safe-prime scan (sieve to 8191, base-2 SPRP, spsp(2) table) "
                                   "of all 2^30 odd candidates in [2^31,2^32) + 2^20 instance tuples "
                                   "(ids 0..2^20-1)",
                       "unit_note": "value = odd candidates per second (scan + tuples in the step; at N>1 the "
                                    "scan phase includes the all-gather of the per-rank counts and lists)"},
-                     "strong", count_launches(w.step), 8)
+                     "strong", launches)
     scan_ms = statistics.median(w.phase["scan"])
     setup_ms = statistics.median(w.phase["setup"])
     line["phases"] = {"scan_ms": scan_ms, "scan_gcandidates_s": (w.hi - w.lo) // 2 / (scan_ms * 1e-3) / 1e9,

@@ -372,6 +372,9 @@ int rsa_abi_version(void);
 int rsa_built_arch(void);
 /* Last CUDA error string seen by this thread (static storage). */
 const char* rsa_last_error(void);
+/* Kernels this library has launched in this process (all entry points; a
+ * launch recorded into a CUDA graph counts once, at capture). */
+uint64_t rsa_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -103,6 +103,7 @@ PROTOTYPES = {
     "rsa_abi_version": (ctypes.c_int, []),
     "rsa_built_arch": (ctypes.c_int, []),
     "rsa_last_error": (ctypes.c_char_p, []),
+    "rsa_launch_count": (c_u64, []),
 }
 
 

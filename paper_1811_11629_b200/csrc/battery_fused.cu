@@ -100,11 +100,24 @@ __device__ void bt_consume_tuples(BtShared& sh, const rsa_battery_spec& sp, uint
     const uint32_t body = len > psi ? len - psi : 0;
     const uint32_t n_t = body / d;
     const uint32_t suf = body - n_t * d;
-    for (uint32_t j = threadIdx.x; j < n_t; j += BT_TB) {
-        bool tie = false;
-        const uint32_t cell = bt_tuple_cell<KIND>(&sh.tile[psi + j * d], sp, &tie);
-        if (KIND == RSA_BT_PERMUTATION && tie) sh.tie = 1;
-        bt_count<KIND>(sh, counts, cell);
+    if constexpr (KIND == RSA_BT_MAX_OF_T) {
+        // long tuples (t = 32): one warp per tuple, lane c holds value c, shuffle max.
+        // (A warp-per-tuple Lehmer rank measured 3.4x slower than one thread per
+        // tuple for the permutation test: profiles/r02_battery_per_test.txt.)
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (uint32_t j = warp; j < n_t; j += BT_TB / 32) {
+            double m = lane < (int)d ? sh.tile[psi + j * d + lane] : 0.0;  // values >= 0: 0 is neutral
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0) bt_count<KIND>(sh, counts, bt_bin(pow(m, (double)d), sp.p2));
+        }
+    } else {
+        for (uint32_t j = threadIdx.x; j < n_t; j += BT_TB) {
+            bool tie = false;
+            const uint32_t cell = bt_tuple_cell<KIND>(&sh.tile[psi + j * d], sp, &tie);
+            if (KIND == RSA_BT_PERMUTATION && tie) sh.tie = 1;
+            bt_count<KIND>(sh, counts, cell);
+        }
     }
     const uint32_t pre = psi < len ? psi : len;
     if (threadIdx.x < pre) slots[b * d + phase + threadIdx.x] = sh.tile[threadIdx.x];
@@ -608,5 +621,5 @@ extern "C" int rsa_battery_chi2_sum(const long long* counts, uint64_t n, double 
     if (g > 148 * 4) g = 148 * 4;
     k_pw_leaves<<<g, 256, 0, st>>>(counts, e, nodes, levels, vals);
     k_pw_combine<<<1, 1024, 0, st>>>(nodes, levels, vals, out);
-    return launch_status("rsa_battery_chi2_sum");
+    return launch_status("rsa_battery_chi2_sum", 3);
 }

@@ -133,6 +133,16 @@ _GRAPH_LOCK = threading.Lock()
 _GRAPH_REPLAY = os.environ.get("RSARAND_GRAPH_REPLAY", "1") != "0"
 
 
+_GRAPH_NET = 0  # kernels executed by graph replays minus the launches recorded at capture
+
+
+def launch_count() -> int:
+    """Kernels of the library executed so far in this process: the C ABI's
+    launch counter corrected for CUDA-graph capture / replay of segmented
+    takes (bench.py's gpu_launches)."""
+    return int(_lib.load().rsa_launch_count()) + _GRAPH_NET
+
+
 def clear_graph_cache() -> None:
     """Drop the captured segmented-fill graphs (and the scratch they hold)."""
     with _GRAPH_LOCK:
@@ -162,9 +172,11 @@ def _segmented_launch(key: tuple, launch, keep: torch.Tensor) -> None:
     if action == "direct":
         launch()
         return
+    global _GRAPH_NET
     if action == "replay":
         with torch.cuda.device(d):
             hit[0].replay()
+        _GRAPH_NET += hit[3]
         return
     # capture on a side stream without torch.cuda.graph's synchronize /
     # gc / empty_cache (only our own kernels are recorded); thread-local
@@ -173,19 +185,23 @@ def _segmented_launch(key: tuple, launch, keep: torch.Tensor) -> None:
     side = torch.cuda.Stream(device=d)
     side.wait_stream(cur)
     g = torch.cuda.CUDAGraph()
+    c0 = int(_lib.load().rsa_launch_count())
     with torch.cuda.device(d), torch.cuda.stream(side):
         g.capture_begin(capture_error_mode="thread_local")
         try:
             scratch = launch()
         finally:
             g.capture_end()
+    captured = int(_lib.load().rsa_launch_count()) - c0
+    _GRAPH_NET -= captured  # recorded, not executed; the replays below execute them
     cur.wait_stream(side)
     with _GRAPH_LOCK:
-        _GRAPHS[key] = (g, keep, scratch)
+        _GRAPHS[key] = (g, keep, scratch, captured)
         if len(_GRAPHS) > _GRAPH_MAX:
             _GRAPHS.popitem(last=False)
     with torch.cuda.device(d):
         g.replay()
+    _GRAPH_NET += captured
 
 
 def next_block_raw(state: VectorState) -> torch.Tensor:

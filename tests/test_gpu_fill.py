@@ -693,3 +693,26 @@ def test_scalar_lookahead_matches_reference_steps(p0):
     rsacore.jump_periods(st, p0, 3)
     want = walk(st.m1, st.m2, st.s, 3)
     assert [rsacore.next_raw(st, p0) for _ in range(3)] == [w[0] for w in want]
+
+
+def test_launch_counter_counts_executed_kernels(p0):
+    """rsa_launch_count (+ vecgen's graph-replay correction) — the evidence
+    behind bench.py's gpu_launches: one bulk fill = 1 kernel; a repeated
+    segmented take = its kernels once per call whether launched directly,
+    captured or replayed."""
+    vecgen.clear_graph_cache()
+    st = R.init_vector(p0, mv=1 << 18)
+    c0 = vecgen.launch_count()
+    R.take_floats(st, (1 << 18) * 4)
+    assert vecgen.launch_count() - c0 == 1
+    s1 = R.init_vector(p0, mv=64)
+    out = torch.empty(64 * 4096, dtype=torch.float64, device="cuda")
+    c0 = vecgen.launch_count()
+    R.take_floats(s1, out.numel(), out=out)  # direct
+    per_call = vecgen.launch_count() - c0
+    assert per_call >= 2
+    for _ in range(3):  # capture + replay, then replays
+        c0 = vecgen.launch_count()
+        R.take_floats(s1, out.numel(), out=out)
+        assert vecgen.launch_count() - c0 == per_call
+    vecgen.clear_graph_cache()
