@@ -451,8 +451,42 @@ def _cpu_cfg5(args):
 
 
 def cpu_baseline_for(config: int, table=None) -> dict | None:
-    """cpu_baseline object of configuration `config` (rank 0, N = 1).
-    `table`: the InstanceTable the GPU run derived (configs 3 and 4)."""
+    """cpu_baseline object of configuration `config` (rank 0, N = 1), measured
+    in a fresh Python process (`python bench_configs.py cpu N [instances]`):
+    worker processes forked from the GPU process (CUDA context, gigabytes of
+    pinned host memory) ran the same numpy work ~40 % slower than the same
+    port in a clean process (profiles/r02_bench_default.json vs the reference
+    arm).  `table`: the InstanceTable the GPU run derived (configs 3 and 4)."""
+    import subprocess
+    import sys
+    insts = []
+    if table is not None and config in (3, 4):
+        n = (os.cpu_count() or 1) * (4 if config == 4 else 1)
+        insts = [[p.p1, p.p2, p.skip.a] for p in (table.params(j) for j in range(n))]
+    res = subprocess.run([sys.executable, os.path.abspath(__file__), "cpu", str(config), json.dumps(insts)],
+                         capture_output=True, text=True)
+    if res.returncode != 0:
+        return {"unavailable": res.stderr.strip().splitlines()[-1] if res.stderr.strip() else "failed"}
+    return json.loads(res.stdout.strip().splitlines()[-1])
+
+
+class _Inst:
+    """The (p1, p2, a) of an instance, shaped like GeneratorParams for the ports."""
+
+    def __init__(self, p1, p2, a):
+        self.p1, self.p2 = p1, p2
+        self.skip = type("S", (), {"a": a})()
+
+
+class _Table:
+    def __init__(self, insts):
+        self.insts = [_Inst(*x) for x in insts]
+
+    def params(self, j):
+        return self.insts[j]
+
+
+def _cpu_baseline_here(config: int, table=None) -> dict | None:
     import multiprocessing as mp
     from oracle import rsa_oracle as O
     procs = os.cpu_count() or 1
@@ -535,3 +569,11 @@ def run_battery_config(args, world, rank, local, dev) -> dict:
                         "n_outside_warn": rep.n_outside_warn, "records": [r.record() for r in rep.reports]},
             "reference_context": ("reference run_battery at budget 2^23 took 57.6 s on one CPU core here "
                                   "(tests/golden/battery.json): 3.35e6 variates/s")}
+
+
+if __name__ == "__main__":
+    import sys
+    if len(sys.argv) >= 3 and sys.argv[1] == "cpu":
+        sys.path.insert(0, ROOT)
+        insts = json.loads(sys.argv[3]) if len(sys.argv) > 3 else []
+        print(json.dumps(_cpu_baseline_here(int(sys.argv[2]), _Table(insts) if insts else None)))
