@@ -491,7 +491,10 @@ def _cpu_baseline_here(config: int, table=None) -> dict | None:
     from oracle import rsa_oracle as O
     procs = os.cpu_count() or 1
     if config == 2:
-        cb = cpu_port_rate()
+        # the box's vCPUs are noisy (+-40 % between back-to-back runs, tools/cpu_probe.py):
+        # best of three, the reference's most favourable figure
+        cb = max((cpu_port_rate() for _ in range(3)), key=lambda r: r["value"])
+        cb["sample"] += " (best of 3 runs)"
         one = cpu_port_rate(procs=1)  # also the single-process figure
         cb["one_process"] = {"value": one["value"], "unit": one["unit"], "cores": 1}
         return cb
