@@ -48,7 +48,7 @@ import bench_configs as C  # noqa: E402
 from bench_configs import EXPONENTS, cpu_port_rate, seeded_m0, w_imad  # noqa: E402,F401
 
 METRIC = "RSA-PRNG Gnumbers/s at 1/2/4/8 B200; % of IMAD/HBM roofline; vs CPU"
-SUB_CONFIGS = (1, 3, 4, 5)
+SUB_CONFIGS = (1, 3, 4, 5, 6)
 MIN_REGION_S = 0.5  # short steps are timed in repeated K-step blocks until the sampler saw this much
 
 
@@ -462,7 +462,16 @@ def run_config5(args, world, rank, local, dev, peak):
     return line, None
 
 
-RUNNERS = {1: run_config1, 2: run_config2, 3: run_config3, 4: run_config4, 5: run_config5}
+def run_config6(args, world, rank, local, dev, peak):
+    """F1: the 23-test battery at budget 1e8 on 2 interleaved
+    streams, consumers fed in registers (bench_configs.run_battery_config)."""
+    line = C.run_battery_config(args, world, rank, local, dev)
+    keep = ("value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "wall_ms_each", "higher_is_better",
+            "scaling", "config", "clocks", "gpu_launches", "battery", "reference_context")
+    return {k: line[k] for k in keep if k in line}, None
+
+
+RUNNERS = {1: run_config1, 2: run_config2, 3: run_config3, 4: run_config4, 5: run_config5, 6: run_config6}
 
 
 def run_gpu(args):
@@ -471,8 +480,7 @@ def run_gpu(args):
     dev = torch.device("cuda", local)
     peak = probe_imad_peak(dev)
     if args.config == 6:
-        from bench_configs import run_battery_config  # noqa: F401  (F1, builder runs only)
-        line = run_battery_config(args, world, rank, local, dev)
+        line = C.run_battery_config(args, world, rank, local, dev)
         tables = {}
     else:
         main_cfg = args.config
@@ -490,7 +498,9 @@ def run_gpu(args):
     if rank == 0 and not args.no_cpu and world == 1:  # the CPU baseline is an N=1, rank-0 measurement
         line["cpu_baseline"] = C.cpu_baseline_for(args.config, tables.get(args.config))
         for c, sub in line.get("configs", {}).items():
-            sub["cpu_baseline"] = C.cpu_baseline_for(int(c), tables.get(int(c)))
+            cb = C.cpu_baseline_for(int(c), tables.get(int(c)))
+            if cb:
+                sub["cpu_baseline"] = cb
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -557,13 +557,16 @@ def run_battery_config(args, world, rank, local, dev) -> dict:
     for _ in range(max(1, args.warmup)):
         stats.run_battery(make, budget=budget)  # warm-up (allocator, cuFFT plans, pinned buffers)
     torch.cuda.synchronize()
+    from bench import launch_count
     walls = []
     with ClockSampler(local) as clk:
         for _ in range(max(1, min(args.steps, 5))):
+            c0 = launch_count()
             t0 = time.perf_counter()
             rep = stats.run_battery(make, budget=budget)
             torch.cuda.synchronize()
             walls.append(time.perf_counter() - t0)
+            launches = launch_count() - c0
     el = statistics.median(walls)
     variates = sum(r.samples for r in rep.reports)
     return {"metric": METRIC, "value": variates / el / 1e9, "unit": "Gvariates/s", "n_gpus": world,
@@ -571,8 +574,8 @@ def run_battery_config(args, world, rank, local, dev) -> dict:
             "wall_ms_each": [w * 1e3 for w in walls], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64 draws -> f64 / low bits", "data": "synthetic: derived stream params",
             "config": {"workload": "config6 (F1): stats.run_battery, 23 tests at budget 1e8 each, "
-                                   "2 interleaved streams (9, 10), Mv=2^16"},
-            "clocks": clk.summary(),
+                                   "2 interleaved streams (9, 10), Mv=2^16; wall time per battery (median)"},
+            "clocks": clk.summary(), "gpu_launches": launches,
             "battery": {"tests": len(rep.reports), "errors": rep.errors, "all_pass": rep.all_pass,
                         "n_outside_warn": rep.n_outside_warn, "records": [r.record() for r in rep.reports]},
             "reference_context": ("reference run_battery at budget 2^23 took 57.6 s on one CPU core here "
