@@ -21,6 +21,7 @@ import torch
 
 from . import _device, _lib, numtheory
 from .skipgen import Q_DEFAULT, Q_DEFAULT_FACTORS, SkipParams, default_skip_params
+from .skipgen import next_skip  # noqa: F401  (re-exported as in rsacore.py of the reference)
 
 DEFAULT_EXPONENT = 9
 MAX_EXPONENT = 257

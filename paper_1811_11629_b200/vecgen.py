@@ -18,9 +18,10 @@ from dataclasses import dataclass, field
 
 import torch
 
-from . import _device, _lib
+from . import _device, _lib, skipgen  # noqa: F401  (skipgen: the reference module's namespace, vecgen.py:1-20)
 from .rsacore import (SKIP_LCG, GeneratorParams, InvalidSeed, device_instance,
-                      instance_flags, validate_params)
+                      instance_flags, validate_params,
+                      MAX_BELOW_ONE, SKIP_CONST, SKIP_UNIT)  # noqa: F401
 
 
 def _empty_u64(dev) -> torch.Tensor:

@@ -53,3 +53,31 @@ def test_reference_unit_tests_pass_against_the_package(files, sel, tmp_path):
     tail = "\n".join(res.stdout.splitlines()[-15:])
     assert res.returncode == 0, tail
     assert " passed" in tail and "failed" not in tail and "error" not in tail.lower(), tail
+
+
+NAMESPACE = r"""
+import importlib, sys
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, {root!r})
+out = {{}}
+for m in ("numtheory", "skipgen", "rsacore", "paramfactory", "vecgen", "stats", ""):
+    ref = importlib.import_module("rsarand" + ("." + m if m else ""))
+    ours = importlib.import_module("paper_1811_11629_b200" + ("." + m if m else ""))
+    names = {{n for n in dir(ref) if not n.startswith("_") and not isinstance(getattr(ref, n), type(sys))
+             or n in ("skipgen", "vecgen", "rsacore", "numtheory", "paramfactory", "stats")}}
+    std = {{"np", "math", "dataclass", "field", "annotations", "Sequence", "Callable", "functools", "special"}}
+    out[m or "rsarand"] = sorted(n for n in names - std if not hasattr(ours, n))
+print(out)
+"""
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_TESTS), reason="the reference is only present in the build container")
+def test_public_names_of_every_reference_module_exist():
+    """Every public name of rsarand and its host-side modules (functions,
+    classes, constants, re-exported modules) exists under the same name in the
+    drop-in package."""
+    res = subprocess.run([sys.executable, "-c", NAMESPACE.format(root=ROOT)], capture_output=True, text=True,
+                         timeout=300, env=dict(os.environ, PYTHONDONTWRITEBYTECODE="1"))
+    assert res.returncode == 0, res.stderr[-2000:]
+    missing = eval(res.stdout.strip().splitlines()[-1])
+    assert all(not v for v in missing.values()), missing
