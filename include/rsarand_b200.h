@@ -306,6 +306,14 @@ int rsa_battery_count(int test, const double* v, uint64_t n, uint32_t p1, uint32
  * phase = position mod d.  The caller fills the parts of boundaries 0 and
  * `tiles` that lie outside the launch (materialised head / tail variates).
  *
+ * RSA_BT_COLLISION (d = 1: urn = cell of one variate among 2^20; d = 20: urn
+ * = the bits (u > 1/2) of 20 consecutive variates; stats.py collision_test):
+ * ball b = test position / d belongs to trial b >> 14; each ball sets its
+ * urn's bit in the trial's 2^20-bit bitmap (spec->aux, uint32[trials][2^15],
+ * zeroed by the caller) and a ball whose bit was already set adds 1 to
+ * counts[trial]; rsa_battery_collision_hist turns those into the test's
+ * histogram.  Collision counts are order-independent.
+ *
  * RSA_BT_GAPS: runs of (u > 1/2) / (u <= 1/2) (stats.py gaps_test): runs that
  * start and end inside one tile are counted (counts[min(len, 64) - 1]); every
  * tile writes records[spec->seg0 + t] for rsa_battery_gaps_stitch.
@@ -321,6 +329,7 @@ typedef struct rsa_battery_spec {
     uint32_t p1, p2;   /* as rsa_battery_count (bins / axis / t)                   */
     uint64_t pos0;     /* test-relative position of the first variate              */
     uint64_t seg0;     /* first boundary slot / gap record of this launch          */
+    uint64_t aux;      /* RSA_BT_COLLISION: device address of the trial bitmaps   */
 } rsa_battery_spec;
 
 typedef struct rsa_gap_record {
@@ -340,6 +349,13 @@ int rsa_battery_gaps_array(const double* v, uint64_t n, const rsa_battery_spec* 
  * position = pos0 + (b - seg0) * RSA_BT_TILE for slot b) is nonzero. */
 int rsa_battery_stitch(const rsa_battery_spec* spec, const double* slots, uint64_t first, uint64_t n,
                        unsigned long long* counts, int* flag, void* stream);
+/* RSA_BT_COLLISION over a device array of n variates holding whole balls
+ * (spec->pos0 = test position of v[0], a multiple of spec->d). */
+int rsa_battery_collision_array(const double* v, uint64_t n, const rsa_battery_spec* spec,
+                                unsigned long long* trial_counts, void* stream);
+/* counts[trial_counts[t]] += 1 for t < trials (the collision histogram). */
+int rsa_battery_collision_hist(const unsigned long long* trial_counts, uint64_t trials,
+                               unsigned long long* counts, void* stream);
 /* Runs that cross tile boundaries, from n_rec records in stream order (the
  * test's open final run is not counted). */
 int rsa_battery_gaps_stitch(const rsa_gap_record* records, uint64_t n_rec,

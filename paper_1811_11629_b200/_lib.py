@@ -50,7 +50,8 @@ FUSED_STAT_DTYPE = np.dtype([("s1", "<f8"), ("s2", "<f8"), ("lag", "<f8"), ("fir
 
 
 class BatterySpec(ctypes.Structure):
-    _fields_ = [("test", c_i32), ("d", c_u32), ("p1", c_u32), ("p2", c_u32), ("pos0", c_u64), ("seg0", c_u64)]
+    _fields_ = [("test", c_i32), ("d", c_u32), ("p1", c_u32), ("p2", c_u32), ("pos0", c_u64), ("seg0", c_u64),
+                ("aux", c_u64)]
 
 
 GAP_RECORD_BYTES = 16  # rsa_gap_record: head, tail, len, bits (uint32 each)
@@ -97,6 +98,8 @@ PROTOTYPES = {
     "rsa_battery_gaps_array": (ctypes.c_int, [c_vp, c_u64, ctypes.POINTER(BatterySpec), c_vp, c_vp, c_vp]),
     "rsa_battery_stitch": (ctypes.c_int, [ctypes.POINTER(BatterySpec), c_vp, c_u64, c_u64, c_vp, c_vp, c_vp]),
     "rsa_battery_gaps_stitch": (ctypes.c_int, [c_vp, c_u64, c_vp, c_vp]),
+    "rsa_battery_collision_array": (ctypes.c_int, [c_vp, c_u64, ctypes.POINTER(BatterySpec), c_vp, c_vp]),
+    "rsa_battery_collision_hist": (ctypes.c_int, [c_vp, c_u64, c_vp, c_vp]),
     "rsa_battery_fourier_bin": (ctypes.c_int, [c_vp, c_u64, c_vp, c_vp, c_vp]),
     "rsa_battery_chi2_scratch_bytes": (c_u64, [c_u64]),
     "rsa_battery_chi2_sum": (ctypes.c_int, [c_vp, c_u64, ctypes.c_double, c_vp, c_vp, c_u64, c_vp]),

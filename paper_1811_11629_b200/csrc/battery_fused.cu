@@ -55,6 +55,10 @@ __device__ __forceinline__ uint32_t bt_tuple_cell(const double* x, const rsa_bat
         double m = x[0];
         for (uint32_t c = 1; c < d; ++c) m = fmax(m, x[c]);
         return bt_bin(pow(m, (double)d), sp.p2);
+    } else if constexpr (KIND == RSA_BT_COLLISION) {  // msb_of_20: bit k = (x_k > 1/2)
+        uint32_t urn = 0;
+        for (uint32_t c = 0; c < d; ++c) urn |= (uint32_t)(x[c] > 0.5) << c;
+        return urn;
     } else {  // RSA_BT_PERMUTATION: Lehmer rank
         uint32_t rank = 0;
         bool eq = false;
@@ -69,6 +73,17 @@ __device__ __forceinline__ uint32_t bt_tuple_cell(const double* x, const rsa_bat
         *tie = eq;
         return rank;
     }
+}
+
+// Collision test: ball `ball` (trial ball >> 14) lands in `urn`; a ball whose
+// urn bit was already set in its trial's 2^20-bit bitmap is a collision.
+constexpr uint32_t BT_COLL_BALLS_LOG = 14, BT_COLL_WORDS = (1u << 20) / 32;
+__device__ __forceinline__ void bt_collide(const rsa_battery_spec& sp, uint64_t ball, uint32_t urn,
+                                           unsigned long long* trial_counts) {
+    const uint64_t trial = ball >> BT_COLL_BALLS_LOG;
+    uint32_t* bm = reinterpret_cast<uint32_t*>(sp.aux) + trial * BT_COLL_WORDS;
+    const uint32_t bit = 1u << (urn & 31);
+    if (atomicOr(&bm[urn >> 5], bit) & bit) atomicAdd(&trial_counts[trial], 1ull);
 }
 
 template <int KIND>
@@ -116,7 +131,8 @@ __device__ void bt_consume_tuples(BtShared& sh, const rsa_battery_spec& sp, uint
             bool tie = false;
             const uint32_t cell = bt_tuple_cell<KIND>(&sh.tile[psi + j * d], sp, &tie);
             if (KIND == RSA_BT_PERMUTATION && tie) sh.tie = 1;
-            bt_count<KIND>(sh, counts, cell);
+            if constexpr (KIND == RSA_BT_COLLISION) bt_collide(sp, (P + psi + j * d) / d, cell, counts);
+            else bt_count<KIND>(sh, counts, cell);
         }
     }
     const uint32_t pre = psi < len ? psi : len;
@@ -223,6 +239,11 @@ k_bat_fused(const rsa_instance* __restrict__ inst, uint32_t S, uint32_t mv, uint
             if constexpr (KIND == RSA_BT_HIST) {
 #pragma unroll
                 for (int r = 0; r < BT_R; ++r) atomicAdd(&counts[bt_bin(v[r], sp.p1)], 1ull);
+            } else if (KIND == RSA_BT_COLLISION && sp.d == 1) {  // top20bits: one ball per variate
+                const uint64_t base = sp.pos0 + (k * C + c) * RSA_BT_TILE;
+#pragma unroll
+                for (int r = 0; r < BT_R; ++r)
+                    bt_collide(sp, base + r * BT_TB + threadIdx.x, bt_bin(v[r], 1u << 20), counts);
             } else {
 #pragma unroll
                 for (int r = 0; r < BT_R; ++r) sh.tile[r * BT_TB + threadIdx.x] = v[r];
@@ -281,7 +302,8 @@ __global__ void k_bat_stitch(const rsa_battery_spec sp, const double* __restrict
         bool tie = false;
         const uint32_t cell = bt_tuple_cell<KIND>(x, sp, &tie);
         if (KIND == RSA_BT_PERMUTATION && tie) sh.tie = 1;
-        bt_count<KIND>(sh, counts, cell);
+        if constexpr (KIND == RSA_BT_COLLISION) bt_collide(sp, (pos - pos % sp.d) / sp.d, cell, counts);
+        else bt_count<KIND>(sh, counts, cell);
     }
     bt_flush<KIND>(sh, sp, counts, flag);
 }
@@ -395,6 +417,7 @@ static void dispatch_bat_e(uint32_t e, unsigned grid, cudaStream_t st, bool low3
 
 static bool bat_tuple_ok(const rsa_battery_spec& sp) {
     switch (sp.test) {
+        case RSA_BT_COLLISION: return (sp.d == 1 || sp.d == 20) && sp.aux != 0;
         case RSA_BT_SERIAL: return sp.d >= 2 && sp.d <= 6 && sp.p2 > 0;
         case RSA_BT_POKER: return sp.d == 5;
         case RSA_BT_MAX_OF_T: return sp.d >= 1 && sp.d <= 32 && sp.p2 > 0 && sp.p2 <= BT_SMALL;
@@ -410,7 +433,9 @@ extern "C" int rsa_battery_fused(const rsa_instance* inst, uint32_t n_inst, uint
     if (!inst || !m1 || !m2 || !s || !spec || !counts || n_inst == 0 || mv == 0 || e == 0) return RSA_EINVAL;
     if (BT_TB % n_inst || ((uint64_t)mv * n_inst) % RSA_BT_TILE) return RSA_EINVAL;
     const rsa_battery_spec sp = *spec;
-    const bool tuple = sp.test != RSA_BT_HIST && sp.test != RSA_BT_GAPS;
+    const bool tuple = sp.test != RSA_BT_HIST && sp.test != RSA_BT_GAPS &&
+                       !(sp.test == RSA_BT_COLLISION && sp.d == 1);
+    if (sp.test == RSA_BT_COLLISION && !bat_tuple_ok(sp)) return RSA_EINVAL;
     if (sp.test == RSA_BT_HIST && (sp.p1 == 0 || sp.d != 1)) return RSA_EINVAL;
     if (sp.test == RSA_BT_GAPS && (sp.d != 1 || !records)) return RSA_EINVAL;
     if (tuple && (!bat_tuple_ok(sp) || !slots)) return RSA_EINVAL;
@@ -428,6 +453,7 @@ extern "C" int rsa_battery_fused(const rsa_instance* inst, uint32_t n_inst, uint
         RSA_BT_CASE(RSA_BT_MAX_OF_T)
         RSA_BT_CASE(RSA_BT_PERMUTATION)
         RSA_BT_CASE(RSA_BT_GAPS)
+        RSA_BT_CASE(RSA_BT_COLLISION)
         default: return RSA_EINVAL;
     }
 #undef RSA_BT_CASE
@@ -450,6 +476,7 @@ extern "C" int rsa_battery_stitch(const rsa_battery_spec* spec, const double* sl
     const rsa_battery_spec sp = *spec;
     if (!bat_tuple_ok(sp) || first < sp.seg0) return RSA_EINVAL;
     if (sp.test == RSA_BT_PERMUTATION && !flag) return RSA_EINVAL;
+    if (sp.test == RSA_BT_COLLISION && sp.d == 1) return RSA_EINVAL;  // single-variate balls never straddle
     if (n == 0) return RSA_OK;
     const unsigned grid = (unsigned)((n + BT_TB - 1) / BT_TB < 148 * 4 ? (n + BT_TB - 1) / BT_TB : 148 * 4);
     cudaStream_t st = as_stream(stream);
@@ -457,6 +484,7 @@ extern "C" int rsa_battery_stitch(const rsa_battery_spec* spec, const double* sl
         case RSA_BT_SERIAL: k_bat_stitch<RSA_BT_SERIAL><<<grid, BT_TB, 0, st>>>(sp, slots, first, n, counts, flag); break;
         case RSA_BT_POKER: k_bat_stitch<RSA_BT_POKER><<<grid, BT_TB, 0, st>>>(sp, slots, first, n, counts, flag); break;
         case RSA_BT_MAX_OF_T: k_bat_stitch<RSA_BT_MAX_OF_T><<<grid, BT_TB, 0, st>>>(sp, slots, first, n, counts, flag); break;
+        case RSA_BT_COLLISION: k_bat_stitch<RSA_BT_COLLISION><<<grid, BT_TB, 0, st>>>(sp, slots, first, n, counts, flag); break;
         default: k_bat_stitch<RSA_BT_PERMUTATION><<<grid, BT_TB, 0, st>>>(sp, slots, first, n, counts, flag); break;
     }
     return launch_status("rsa_battery_stitch");
@@ -478,6 +506,28 @@ extern "C" int rsa_battery_fourier_bin(const double* coeff, uint64_t n, const do
     if (grid > 148 * 8) grid = 148 * 8;
     k_bat_fourier_bin<<<grid, 256, 0, as_stream(stream)>>>(coeff, n, edges, counts);
     return launch_status("rsa_battery_fourier_bin");
+}
+
+// Collision balls from a materialised array of whole balls.
+__global__ void k_bat_collision_array(const double* __restrict__ v, uint64_t balls, const rsa_battery_spec sp,
+                                      unsigned long long* __restrict__ trial_counts) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < balls;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t urn;
+        if (sp.d == 1) urn = bt_bin(v[j], 1u << 20);
+        else {
+            urn = 0;
+            for (uint32_t c = 0; c < sp.d; ++c) urn |= (uint32_t)(v[j * sp.d + c] > 0.5) << c;
+        }
+        bt_collide(sp, sp.pos0 / sp.d + j, urn, trial_counts);
+    }
+}
+
+__global__ void k_bat_collision_hist(const unsigned long long* __restrict__ trial_counts, uint64_t trials,
+                                     unsigned long long* __restrict__ counts) {
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < trials;
+         t += (uint64_t)gridDim.x * blockDim.x)
+        atomicAdd(&counts[trial_counts[t]], 1ull);
 }
 
 // ---- chi-square sum in numpy's order -------------------------------------------
@@ -622,4 +672,27 @@ extern "C" int rsa_battery_chi2_sum(const long long* counts, uint64_t n, double 
     k_pw_leaves<<<g, 256, 0, st>>>(counts, e, nodes, levels, vals);
     k_pw_combine<<<1, 1024, 0, st>>>(nodes, levels, vals, out);
     return launch_status("rsa_battery_chi2_sum", 3);
+}
+
+extern "C" int rsa_battery_collision_array(const double* v, uint64_t n, const rsa_battery_spec* spec,
+                                           unsigned long long* trial_counts, void* stream) {
+    if ((!v && n) || !spec || !trial_counts) return RSA_EINVAL;
+    const rsa_battery_spec sp = *spec;
+    if (sp.test != RSA_BT_COLLISION || !bat_tuple_ok(sp) || n % sp.d || sp.pos0 % sp.d) return RSA_EINVAL;
+    if (n == 0) return RSA_OK;
+    const uint64_t balls = n / sp.d;
+    unsigned grid = grid_for(balls, 256);
+    if (grid > 148 * 8) grid = 148 * 8;
+    k_bat_collision_array<<<grid, 256, 0, as_stream(stream)>>>(v, balls, sp, trial_counts);
+    return launch_status("rsa_battery_collision_array");
+}
+
+extern "C" int rsa_battery_collision_hist(const unsigned long long* trial_counts, uint64_t trials,
+                                          unsigned long long* counts, void* stream) {
+    if ((!trial_counts && trials) || !counts) return RSA_EINVAL;
+    if (trials == 0) return RSA_OK;
+    unsigned grid = grid_for(trials, 256);
+    if (grid > 148 * 8) grid = 148 * 8;
+    k_bat_collision_hist<<<grid, 256, 0, as_stream(stream)>>>(trial_counts, trials, counts);
+    return launch_status("rsa_battery_collision_hist");
 }

@@ -168,3 +168,21 @@ def test_device_chi2_sum_is_numpys(n):
     want = np.square(counts - e).sum()
     got = stats._chi2_sum_device(torch.as_tensor(counts, device="cuda"), e)
     assert got == float(want)
+
+
+@pytest.mark.parametrize("variant,trials", [("top20bits", 40), ("msb_of_20", 18)])
+@pytest.mark.parametrize("k,mv,sel,pre", CASES)
+def test_fused_collisions_equal_materialised(variant, trials, k, mv, sel, pre):
+    """Collision balls fed in registers (per-trial bitmaps in device memory,
+    20-variate balls across tiles through the boundary slots) give the
+    materialised path's exact per-trial collision histogram."""
+    a, b = make(k, mv, sel), make(k, mv, sel)
+    if pre:
+        a.take(pre)
+        b.take(pre)
+    d = 20 if variant == "msb_of_20" else 1
+    assert stats._fused_plan(a, trials * stats.COLLISION_BALLS * d) is not None
+    ra = stats.collision_test(a, variant, trials)
+    rb = stats.collision_test(Proxy(b), variant, trials)
+    assert ra.result == rb.result and ra.samples == rb.samples
+    assert torch.equal(a.take(3 * k * mv + 1), b.take(3 * k * mv + 1))
