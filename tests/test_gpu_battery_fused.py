@@ -170,7 +170,7 @@ def test_device_chi2_sum_is_numpys(n):
     assert got == float(want)
 
 
-@pytest.mark.parametrize("variant,trials", [("top20bits", 40), ("msb_of_20", 18)])
+@pytest.mark.parametrize("variant,trials", [("top20bits", 64), ("msb_of_20", 64)])
 @pytest.mark.parametrize("k,mv,sel,pre", CASES)
 def test_fused_collisions_equal_materialised(variant, trials, k, mv, sel, pre):
     """Collision balls fed in registers (per-trial bitmaps in device memory,
