@@ -141,6 +141,11 @@ int rsa_scalar_lookahead(const rsa_instance* inst, uint64_t m1, uint64_t m2, uin
 /* floats_from_raw (vecgen.py:103-107): out[j] = min(fl(raw[j])/fl(n), 1-2^-53). */
 int rsa_floats_from_raw(const uint64_t* raw, uint64_t count, uint64_t n, double* out,
                         void* stream);
+/* The same map by the 4-op quotient the fused kernels use (double-double
+ * reciprocal + one Markstein step): an independent cross-check of that path,
+ * bit-identical to rsa_floats_from_raw. */
+int rsa_floats_from_raw_dd(const uint64_t* raw, uint64_t count, uint64_t n, double* out,
+                           void* stream);
 
 /* Lane initialisation, vecgen.init_vector (vecgen.py:44-69) for every instance.
  * lcg mode: s[i*mv+g] = s0 * a^(g*floor((q-1)/mv)) mod q

@@ -71,6 +71,7 @@ PROTOTYPES = {
     "rsa_fill": (ctypes.c_int, [c_vp, c_u32, c_u32, c_u64, c_u32, c_u32, c_vp, c_vp, c_vp,
                                 c_vp, c_vp, c_u64, c_vp]),
     "rsa_floats_from_raw": (ctypes.c_int, [c_vp, c_u64, c_u64, c_vp, c_vp]),
+    "rsa_floats_from_raw_dd": (ctypes.c_int, [c_vp, c_u64, c_u64, c_vp, c_vp]),
     "rsa_skip_array": (ctypes.c_int, [c_vp, c_u64, c_u64, c_u64, c_vp, c_vp]),
     "rsa_fill_segments": (c_u64, [c_u64, c_u64]),
     "rsa_scalar_lookahead": (ctypes.c_int, [c_vp, c_u64, c_u64, c_u64, c_u32, c_u32, c_u32, c_vp, c_vp]),

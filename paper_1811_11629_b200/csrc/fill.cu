@@ -123,13 +123,15 @@ k_fill_general(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t tota
     s[lane] = L.s;
 }
 
+template <bool DD>
 __global__ void k_floats_from_raw(const uint64_t* __restrict__ raw, uint64_t count, uint64_t n,
                                   double* __restrict__ out) {
     double nf = __ull2double_rn(n);
     double nr = __drcp_rn(nf);
+    double nl = recip_lo(nf, nr);
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count;
          j += (uint64_t)gridDim.x * blockDim.x)
-        out[j] = to_unit(raw[j], nf, nr);
+        out[j] = DD ? to_unit_dd(raw[j], nf, nr, nl) : to_unit(raw[j], nf, nr);
 }
 
 // out[j] = a * s[j] mod q: skipgen.next_skip_array (skipgen.py:108-116), one
@@ -305,8 +307,19 @@ extern "C" int rsa_floats_from_raw(const uint64_t* raw, uint64_t count, uint64_t
     if (count == 0) return RSA_OK;
     unsigned grid = grid_for(count, 256);
     if (grid > 148 * 16) grid = 148 * 16;
-    k_floats_from_raw<<<grid, 256, 0, as_stream(stream)>>>(raw, count, n, out);
+    k_floats_from_raw<false><<<grid, 256, 0, as_stream(stream)>>>(raw, count, n, out);
     return launch_status("rsa_floats_from_raw");
+}
+
+extern "C" int rsa_floats_from_raw_dd(const uint64_t* raw, uint64_t count, uint64_t n, double* out,
+                                      void* stream) {
+    if ((!raw || !out) && count) return RSA_EINVAL;
+    if (n == 0) return RSA_EINVAL;
+    if (count == 0) return RSA_OK;
+    unsigned grid = grid_for(count, 256);
+    if (grid > 148 * 16) grid = 148 * 16;
+    k_floats_from_raw<true><<<grid, 256, 0, as_stream(stream)>>>(raw, count, n, out);
+    return launch_status("rsa_floats_from_raw_dd");
 }
 
 extern "C" int rsa_skip_array(const uint64_t* s, uint64_t count, uint64_t a, uint64_t q, uint64_t* out,

@@ -214,10 +214,9 @@ def test_clamp_and_float_map(p0, golden_vectors):
         got = np.empty_like(want)
         ct = torch.from_numpy(c).cuda()
         out = torch.empty(len(c), dtype=torch.float64, device="cuda")
-        _lib.call("rsa_floats_from_raw", ct.data_ptr(), len(c), n, out.data_ptr(),
-                  torch.cuda.current_stream().cuda_stream)
-        got = u64np(out)
-        assert np.array_equal(got, want), n
+        for fn in ("rsa_floats_from_raw", "rsa_floats_from_raw_dd"):  # 5-op and 4-op quotients
+            _lib.call(fn, ct.data_ptr(), len(c), n, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+            assert np.array_equal(u64np(out), want), (fn, n)
 
 
 def test_lane_seeds(p0, golden_vectors):
@@ -365,8 +364,8 @@ def test_capi_argument_errors(p0):
 
 
 def test_float_map_many_moduli_and_near_midpoints(golden_streams):
-    """The reciprocal + Markstein float map against IEEE division for 512
-    derived moduli: random ciphertexts and ciphertexts whose quotient sits
+    """The reciprocal + Markstein float maps (5-op, and the 4-op double-double
+    form of the fused kernels) against IEEE division for 512 derived moduli: random ciphertexts and ciphertexts whose quotient sits
     next to a rounding midpoint (the hardest inputs for a correctly rounded
     divide)."""
     from paper_1811_11629_b200 import _device
@@ -385,8 +384,9 @@ def test_float_map_many_moduli_and_near_midpoints(golden_streams):
         want = np.minimum(c.astype(np.float64) / float(n), rsacore.MAX_BELOW_ONE)
         ct = torch.from_numpy(c).to(d)
         out = torch.empty(len(c), dtype=torch.float64, device=d)
-        _lib.call("rsa_floats_from_raw", ct.data_ptr(), len(c), int(n), out.data_ptr(), _device.stream(d))
-        assert np.array_equal(u64np(out), want), n
+        for fn in ("rsa_floats_from_raw", "rsa_floats_from_raw_dd"):  # 5-op and 4-op quotients
+            _lib.call(fn, ct.data_ptr(), len(c), int(n), out.data_ptr(), _device.stream(d))
+            assert np.array_equal(u64np(out), want), (fn, n)
 
 
 # lanes x blocks <= 2^23 take K1p (one thread per draw), larger ones K1s (segments)
