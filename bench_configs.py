@@ -557,18 +557,19 @@ def run_battery_config(args, world, rank, local, dev) -> dict:
     for _ in range(max(1, args.warmup)):
         stats.run_battery(make, budget=budget)  # warm-up (allocator, cuFFT plans, pinned buffers)
     torch.cuda.synchronize()
-    from bench import launch_count
+    from bench import barrier_sync, launch_count, max_over_ranks
     walls = []
     with ClockSampler(local) as clk:
         for _ in range(max(1, min(args.steps, 5))):
+            barrier_sync(world)
             c0 = launch_count()
             t0 = time.perf_counter()
             rep = stats.run_battery(make, budget=budget)
             torch.cuda.synchronize()
-            walls.append(time.perf_counter() - t0)
+            walls.append(max_over_ranks(time.perf_counter() - t0, world))  # every rank runs its own battery
             launches = launch_count() - c0
     el = statistics.median(walls)
-    variates = sum(r.samples for r in rep.reports)
+    variates = world * sum(r.samples for r in rep.reports)
     return {"metric": METRIC, "value": variates / el / 1e9, "unit": "Gvariates/s", "n_gpus": world,
             "steps": len(walls), "warmup": max(1, args.warmup), "ms_per_step": el * 1e3,
             "wall_ms_each": [w * 1e3 for w in walls], "higher_is_better": True, "scaling": "weak",
