@@ -61,56 +61,111 @@ def peaks() -> dict:
 
 
 # ---------------------------------------------------------------------------
-# clocks sampler (nvidia-smi during the timed region)
+# clocks sampler (NVML every 5 ms during the timed region; nvidia-smi fallback)
+
+_REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
 
 class ClockSampler:
+    """SM clock and throttle reasons sampled while the timed region runs.
+
+    NVML (pynvml) is polled from a thread every 5 ms, so even a 0.1 s region
+    yields ~20 samples; without NVML, `nvidia-smi -lms 50` as the recipe's
+    clocks line.  summary() -> {sm_mhz (median), sm_max_mhz, reasons, samples}.
+    """
     FIELDS = ("clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
               "clocks_event_reasons.sw_power_cap")
+    PERIOD_S = 0.005
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines: list[str] = []
+        self.nvml = None
+        self.rows: list[tuple] = []  # (sm_mhz, max_mhz, reason names)
         self._first = threading.Event()
+        self._stop = threading.Event()
+        self.source = "none"
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={','.join(self.FIELDS)}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-            self._first.wait(timeout=5.0)  # sampling has started before the timed region
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.handle = self._nvml_handle(pynvml)
+            self._bits = (pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                          pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM))
+            self.source = "nvml/5ms"
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+        except Exception:
+            self.nvml = None
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={','.join(self.FIELDS)}",
+                     "--format=csv,noheader,nounits", "-lms", "50"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.source = "nvidia-smi/50ms"
+                self.thread = threading.Thread(target=self._read, daemon=True)
+            except OSError:
+                self.proc = None
+                return self
+        self.thread.start()
+        self._first.wait(timeout=5.0)  # sampling has started before the timed region
         return self
+
+    def _nvml_handle(self, pynvml):
+        # the CUDA device this rank uses, matched by PCI bus id (CUDA_VISIBLE_DEVICES may remap)
+        try:
+            import torch
+            props = torch.cuda.get_device_properties(self.index)
+            bus = "%08x:%02x:%02x.0" % (props.pci_domain_id, props.pci_bus_id, props.pci_device_id)
+            return pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:
+            return pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _poll(self):
+        pynvml = self.nvml
+        while not self._stop.is_set():
+            try:
+                sm = float(pynvml.nvmlDeviceGetClockInfo(self.handle, pynvml.NVML_CLOCK_SM))
+                bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+                self.rows.append((sm, self.max_mhz, tuple(n for n, b in zip(_REASONS, self._bits) if bits & b)))
+            except Exception:
+                pass
+            self._first.set()
+            self._stop.wait(self.PERIOD_S)
+        self._first.set()
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            r = [x.strip() for x in line.split(",")]
+            if len(r) >= 6 and r[0].replace(".", "").isdigit():
+                mx = float(r[1]) if r[1].replace(".", "").isdigit() else None
+                self.rows.append((float(r[0]), mx, tuple(n for i, n in enumerate(_REASONS)
+                                                         if r[2 + i].lower() == "active")))
             self._first.set()
         self._first.set()
 
     def __exit__(self, *exc):
+        self._stop.set()
         if self.proc is not None:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        elif self.nvml is not None:
+            self.thread.join(timeout=1.0)
 
     def summary(self) -> dict:
-        rows = [[x.strip() for x in ln.split(",")] for ln in self.lines if ln.count(",") >= 5]
+        rows = list(self.rows)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+        mx = [r[1] for r in rows if r[1] is not None]
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted({n for r in rows for n in r[2]}), "samples": len(rows),
+                "source": self.source}
 
 
 # ---------------------------------------------------------------------------
