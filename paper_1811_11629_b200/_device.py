@@ -8,9 +8,17 @@ import torch
 from ._lib import RsaCudaError
 
 
+_CUDA_OK = False  # set once a CUDA device was found (the check costs ~1 us per call)
+
+
 def device(dev=None) -> torch.device:
-    if not torch.cuda.is_available():
-        raise RsaCudaError("rsarand_b200 needs a CUDA device (sm_100a); none is available")
+    global _CUDA_OK
+    if _CUDA_OK and type(dev) is torch.device and dev.type == "cuda" and dev.index is not None:
+        return dev  # the hot path: a VectorState's own tensor device
+    if not _CUDA_OK:
+        if not torch.cuda.is_available():
+            raise RsaCudaError("rsarand_b200 needs a CUDA device (sm_100a); none is available")
+        _CUDA_OK = True
     if dev is None:
         return torch.device("cuda", torch.cuda.current_device())
     d = torch.device(dev)
@@ -19,7 +27,13 @@ def device(dev=None) -> torch.device:
     return torch.device("cuda", d.index if d.index is not None else torch.cuda.current_device())
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream(dev: torch.device) -> int:
+    """cudaStream_t of torch's current stream on `dev` (no Stream object built)."""
+    if _raw_stream is not None and dev.index is not None:
+        return _raw_stream(dev.index)
     return torch.cuda.current_stream(dev).cuda_stream
 
 

@@ -150,5 +150,14 @@ def check(rc: int, what: str) -> None:
         raise RsaCudaError(f"{what} failed with status {rc}: {err}")
 
 
+_FN: dict = {}  # name -> (library, typed entry point): skips a getattr per call
+
+
 def call(name: str, *args) -> None:
-    check(getattr(load(), name)(*args), name)
+    lib = _LIB if _LIB is not None else load()
+    hit = _FN.get(name)
+    if hit is None or hit[0] is not lib:
+        hit = _FN[name] = (lib, getattr(lib, name))
+    rc = hit[1](*args)
+    if rc != RSA_OK:
+        check(rc, name)

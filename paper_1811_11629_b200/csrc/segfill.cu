@@ -246,33 +246,65 @@ struct PdLane {
     uint64_t m1, m2, s_end;  // initial residues (snapshot), skip after the last draw
 };
 
-// pass 1: CTA (lane, c) covers segments [c*PD_BLOCK, (c+1)*PD_BLOCK) of lane
+// Segment starts: thread j needs s_0 a^(PD_SEG j) mod q.  The CTA's first
+// PD_TBITS threads build T[k] = a^(PD_SEG 2^k) (4 + k squarings each, in
+// parallel) and every thread multiplies the entries of its set bits: ~log2(j)/2
+// products instead of a per-thread square-and-multiply over a^PD_SEG
+// (k_pd_skips issued 3.9k instructions per 16-draw segment that way).
+constexpr int PD_TBITS = 20;  // nseg <= RSA_PD_MAX / PD_SEG = 2^19
+constexpr int PD_SEG_LOG = 4;
+static_assert(PD_SEG == 1 << PD_SEG_LOG, "segment length is a power of two");
+constexpr int PD_STAGE = PD_SEG + 1;  // staging row pitch (uint2): 2-way bank conflicts at most
+
+// pass 1: CTA (lane, c) covers segments [c*PD_BLOCK, (c+1)*PD_BLOCK) of lane,
+// i.e. draws [c*PD_BLOCK*PD_SEG, ...); increments are staged in shared memory
+// and written back coalesced (one thread per 16 consecutive uint2 would touch
+// 32 lines per warp store)
 __global__ void __launch_bounds__(PD_BLOCK)
 k_pd_skips(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t blocks, uint64_t nseg,
-           uint64_t cta_per_lane, const uint64_t* __restrict__ m1, const uint64_t* __restrict__ m2,
+           uint32_t cta_per_lane, const uint64_t* __restrict__ m1, const uint64_t* __restrict__ m2,
            const uint64_t* __restrict__ s, uint2* __restrict__ inc, uint2* __restrict__ segpre,
            uint2* __restrict__ ctot, PdLane* __restrict__ snap) {
-    const uint64_t lane = blockIdx.x / cta_per_lane, c = blockIdx.x - lane * cta_per_lane;
-    const uint64_t j = c * PD_BLOCK + threadIdx.x;
+    __shared__ uint64_t T[PD_TBITS];
+    __shared__ uint2 stage[PD_BLOCK * PD_STAGE];
+    const uint32_t lane = blockIdx.x / cta_per_lane, c = blockIdx.x - lane * cta_per_lane;
+    const uint64_t j = (uint64_t)c * PD_BLOCK + threadIdx.x;
     const FastInst P = load_fast(inst + lane / mv);
+    const int nbits = 64 - __clzll(nseg > 1 ? nseg - 1 : 1);  // bits of the largest segment index
+    if (threadIdx.x < nbits) {
+        uint64_t x = P.a;
+        for (uint32_t k = 0; k < PD_SEG_LOG + threadIdx.x; ++k) x = mulmod_q63(x, x);
+        T[threadIdx.x] = x;
+    }
+    __syncthreads();
     uint32_t a1 = 0, a2 = 0;
     if (j < nseg) {
         const uint64_t k0 = j * PD_SEG, len = min((uint64_t)PD_SEG, blocks - k0);
-        uint64_t sk = seg_start(s[lane], pow_q63(P.a, PD_SEG), j);
-        uint2* out = inc + lane * blocks + k0;
-        for (uint64_t k = 0; k < len; ++k) {
-            sk = skip_q63(sk, P.a);
-            const uint32_t r1 = mont_redc(sk, P.p1, P.p1_inv), r2 = mont_redc(sk, P.p2, P.p2_inv);
-            out[k] = make_uint2(r1, r2);
-            a1 = add_mod(a1, r1, P.p1);
-            a2 = add_mod(a2, r2, P.p2);
+        uint64_t sk = s[lane];
+        for (int k = 0; k < nbits; ++k)
+            if ((j >> k) & 1) sk = mulmod_q63(sk, T[k]);
+        uint2* row = stage + threadIdx.x * PD_STAGE;
+#pragma unroll
+        for (int k = 0; k < PD_SEG; ++k) {
+            if (k < len) {
+                sk = skip_q63(sk, P.a);
+                const uint32_t r1 = mont_redc(sk, P.p1, P.p1_inv), r2 = mont_redc(sk, P.p2, P.p2_inv);
+                row[k] = make_uint2(r1, r2);
+                a1 = add_mod(a1, r1, P.p1);
+                a2 = add_mod(a2, r2, P.p2);
+            }
         }
         if (j == nseg - 1) snap[lane] = PdLane{m1[lane], m2[lane], sk};
     }
     uint32_t t1, t2;
-    block_excl_scan2(a1, a2, P.p1, P.p2, &t1, &t2);
-    if (j < nseg) segpre[lane * nseg + j] = make_uint2(a1, a2);
+    block_excl_scan2(a1, a2, P.p1, P.p2, &t1, &t2);  // (its __syncthreads also orders the staging)
+    if (j < nseg) segpre[(uint64_t)lane * nseg + j] = make_uint2(a1, a2);
     if (threadIdx.x == 0) ctot[blockIdx.x] = make_uint2(t1, t2);
+    const uint64_t d0 = (uint64_t)c * PD_BLOCK * PD_SEG;
+    const uint32_t n = (uint32_t)min((uint64_t)PD_BLOCK * PD_SEG, blocks - d0);
+    uint2* out = inc + (uint64_t)lane * blocks + d0;
+    for (uint32_t e = threadIdx.x; e < n; e += PD_BLOCK)
+        out[e] = stage[(e >> PD_SEG_LOG) * PD_STAGE + (e & (PD_SEG - 1))];
 }
 
 // pass 2: CTA (lane, b) covers draws [b*PD_CTA2, (b+1)*PD_CTA2) of lane,
@@ -281,24 +313,34 @@ k_pd_skips(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t blocks, 
 template <uint32_t E, bool RAW, bool F64>
 __global__ void __launch_bounds__(PD_BLOCK)
 k_pd_draws(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t blocks, uint64_t nseg,
-           uint64_t cta1_per_lane, uint64_t cta_per_lane, const uint2* __restrict__ inc,
+           uint32_t cta1_per_lane, uint32_t cta_per_lane, const uint2* __restrict__ inc,
            const uint2* __restrict__ segpre, const uint2* __restrict__ ctot, const PdLane* __restrict__ snap,
            uint64_t* __restrict__ m1, uint64_t* __restrict__ m2, uint64_t* __restrict__ s,
            uint64_t* __restrict__ raw, double* __restrict__ f64, uint64_t inst_stride) {
+    static_assert(PD_DPT == 4, "two 16-byte increment loads per thread");
     __shared__ uint32_t off1, off2;
-    const uint64_t lane = blockIdx.x / cta_per_lane, b = blockIdx.x - lane * cta_per_lane;
-    const uint64_t i = lane / mv;
-    const uint32_t g = (uint32_t)(lane - i * mv);
+    const uint32_t lane = blockIdx.x / cta_per_lane, b = blockIdx.x - lane * cta_per_lane;
+    const uint32_t i = lane / mv;
+    const uint32_t g = lane - i * mv;
     const FastInst P = load_fast(inst + i);
     const int wl = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint64_t d0 = b * PD_CTA2 + (uint64_t)threadIdx.x * PD_DPT;  // this thread's first draw
+    const uint64_t d0 = (uint64_t)b * PD_CTA2 + (uint64_t)threadIdx.x * PD_DPT;  // this thread's first draw
     if (threadIdx.x < 32) {  // the lane's pass-1 CTA totals before this CTA's pass-1 CTA
-        const uint64_t c1 = (b * PD_CTA2 / PD_SEG) / PD_BLOCK;
+        const uint32_t c1 = (uint32_t)(((uint64_t)b * PD_CTA2 / PD_SEG) / PD_BLOCK);
+        const uint2* ct = ctot + (uint64_t)lane * cta1_per_lane;
         uint32_t o1 = 0, o2 = 0;
-        for (uint64_t k = threadIdx.x; k < c1; k += 32) {
-            const uint2 v = ctot[lane * cta1_per_lane + k];
-            o1 = add_mod(o1, v.x, P.p1);
-            o2 = add_mod(o2, v.y, P.p2);
+        for (uint32_t k0 = 0; k0 < c1; k0 += 8 * 32) {  // 8 loads in flight per thread
+            uint2 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t k = k0 + u * 32 + threadIdx.x;
+                v[u] = k < c1 ? ct[k] : make_uint2(0u, 0u);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                o1 = add_mod(o1, v[u].x, P.p1);
+                o2 = add_mod(o2, v[u].y, P.p2);
+            }
         }
 #pragma unroll
         for (int dd = 16; dd > 0; dd >>= 1) {
@@ -308,13 +350,22 @@ k_pd_draws(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t blocks, 
         if (threadIdx.x == 0) { off1 = o1; off2 = o2; }
     }
     // this thread's increments (past the end: zero) and their running sums
+    uint2 v[PD_DPT];
+    const uint2* src = inc + (uint64_t)lane * blocks + d0;
+    if (d0 + PD_DPT <= blocks && ((uintptr_t)src & 15) == 0) {
+        const uint4 w0 = __ldg(reinterpret_cast<const uint4*>(src)), w1 = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+        v[0] = make_uint2(w0.x, w0.y); v[1] = make_uint2(w0.z, w0.w);
+        v[2] = make_uint2(w1.x, w1.y); v[3] = make_uint2(w1.z, w1.w);
+    } else {
+#pragma unroll
+        for (int k = 0; k < PD_DPT; ++k) v[k] = d0 + k < blocks ? src[k] : make_uint2(0u, 0u);
+    }
     uint32_t q1[PD_DPT], q2[PD_DPT];
     uint32_t t1 = 0, t2 = 0;
 #pragma unroll
     for (int k = 0; k < PD_DPT; ++k) {
-        const uint2 v = d0 + k < blocks ? inc[lane * blocks + d0 + k] : make_uint2(0u, 0u);
-        t1 = add_mod(t1, v.x, P.p1);
-        t2 = add_mod(t2, v.y, P.p2);
+        t1 = add_mod(t1, v[k].x, P.p1);
+        t2 = add_mod(t2, v[k].y, P.p2);
         q1[k] = t1;
         q2[k] = t2;
     }
@@ -322,14 +373,16 @@ k_pd_draws(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t blocks, 
     warp_scan2(e1, e2, P.p1, P.p2, wl);  // inclusive over the warp's threads
     e1 = sub_mod(e1, t1, P.p1);          // exclusive: the warp's draws before this thread
     e2 = sub_mod(e2, t2, P.p2);
+    // loads that do not need warp 0's offsets are issued before the barrier
+    const bool live = d0 < blocks;
+    const PdLane z = live ? snap[lane] : PdLane{0, 0, 0};
+    const uint2 sp = live ? segpre[(uint64_t)lane * nseg + (d0 - (uint64_t)wl * PD_DPT) / PD_SEG] : make_uint2(0u, 0u);
     __syncthreads();
-    if (d0 >= blocks) return;
-    const PdLane z = snap[lane];
-    const uint2 sp = segpre[lane * nseg + (b * PD_CTA2 + (uint64_t)wid * 32 * PD_DPT) / PD_SEG];
+    if (!live) return;
     // message before this thread's draws: x0 + pass-1 CTA offset + segment prefix + warp prefix
     const uint32_t b1 = add_mod(add_mod(add_mod(mont_redc(z.m1, P.p1, P.p1_inv), off1, P.p1), sp.x, P.p1), e1, P.p1);
     const uint32_t b2 = add_mod(add_mod(add_mod(mont_redc(z.m2, P.p2, P.p2_inv), off2, P.p2), sp.y, P.p2), e2, P.p2);
-    const uint64_t o = i * inst_stride + d0 * mv + g;
+    const uint64_t o = (uint64_t)i * inst_stride + d0 * mv + g;
     with_garner(P, [&](auto gf) {
         constexpr bool GF = decltype(gf)::value;
 #pragma unroll
@@ -464,7 +517,7 @@ static void launch_pd(unsigned grid, cudaStream_t st, const rsa_instance* inst, 
     const uint2* pre = reinterpret_cast<const uint2*>(sc + Lo.segpre);
     const uint2* tot = reinterpret_cast<const uint2*>(sc + Lo.ctot);
     const PdLane* snap = reinterpret_cast<const PdLane*>(sc + Lo.snap);
-#define RSA_PD(R, F) k_pd_draws<E, R, F><<<grid, PD_BLOCK, 0, st>>>(inst, mv, blocks, Lo.nseg, Lo.cta1, Lo.cta2, inc, pre, tot, snap, m1, m2, s, raw, f64, stride)
+#define RSA_PD(R, F) k_pd_draws<E, R, F><<<grid, PD_BLOCK, 0, st>>>(inst, mv, blocks, Lo.nseg, (uint32_t)Lo.cta1, (uint32_t)Lo.cta2, inc, pre, tot, snap, m1, m2, s, raw, f64, stride)
     if (raw && f64) RSA_PD(true, true);
     else if (raw) RSA_PD(true, false);
     else RSA_PD(false, true);
@@ -498,7 +551,7 @@ extern "C" int rsa_fill_segmented(const rsa_instance* inst, uint32_t n_inst, uin
         if (!grid_fits(lanes * Lo.cta1 * PD_BLOCK, PD_BLOCK) || !grid_fits(lanes * Lo.cta2 * PD_BLOCK, PD_BLOCK))
             return RSA_EINVAL;
         k_pd_skips<<<(unsigned)(lanes * Lo.cta1), PD_BLOCK, 0, st>>>(
-            inst, mv, blocks, Lo.nseg, Lo.cta1, m1, m2, s, reinterpret_cast<uint2*>(sc + Lo.inc),
+            inst, mv, blocks, Lo.nseg, (uint32_t)Lo.cta1, m1, m2, s, reinterpret_cast<uint2*>(sc + Lo.inc),
             reinterpret_cast<uint2*>(sc + Lo.segpre), reinterpret_cast<uint2*>(sc + Lo.ctot),
             reinterpret_cast<PdLane*>(sc + Lo.snap));
         if ((rc = launch_status("rsa_fill_segmented(per-draw skips)"))) return rc;

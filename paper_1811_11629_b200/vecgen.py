@@ -11,6 +11,8 @@ chunk computes.
 
 from __future__ import annotations
 
+import functools
+
 import os
 import threading
 from collections import OrderedDict
@@ -85,6 +87,14 @@ def init_vector(params: GeneratorParams, m0: int = 0, s0: int = 1, mv: int = 1,
     return VectorState(params=params, mv=mv, m1=m1, m2=m2, s=s)
 
 
+@functools.lru_cache(maxsize=1024)
+def _segment_plan(lanes: int, blocks: int) -> tuple[int, int]:
+    """(segments per lane, scratch bytes) of rsa_fill_segmented for this shape."""
+    L = _lib.load()
+    nseg = int(L.rsa_fill_segments(lanes, blocks))
+    return nseg, int(L.rsa_fill_segmented_scratch_bytes(lanes, blocks)) if nseg > 1 else 0
+
+
 def _fill(state: VectorState, blocks: int, raw: torch.Tensor | None, f64: torch.Tensor | None) -> None:
     """Advance all lanes `blocks` steps, writing block-major outputs.  Few
     lanes x many blocks (the scalar stream, Mv = 64) take the segmented kernel
@@ -96,12 +106,10 @@ def _fill(state: VectorState, blocks: int, raw: torch.Tensor | None, f64: torch.
     d = state.device
     inst = device_instance(p, d)
     flags = instance_flags(p)
-    L = _lib.load()
     out_r = raw.data_ptr() if raw is not None else None
     out_f = f64.data_ptr() if f64 is not None else None
-    nseg = int(L.rsa_fill_segments(state.mv, blocks))
+    nseg, nbytes = _segment_plan(state.mv, blocks)
     if nseg > 1 and flags & _lib.RSA_FLAG_FAST and (raw is not None or f64 is not None):
-        nbytes = int(L.rsa_fill_segmented_scratch_bytes(state.mv, blocks))
 
         def launch():
             scratch = torch.empty(nbytes, dtype=torch.uint8, device=d)
@@ -175,8 +183,11 @@ def _segmented_launch(key: tuple, launch, keep: torch.Tensor) -> None:
         return
     global _GRAPH_NET
     if action == "replay":
-        with torch.cuda.device(d):
+        if torch.cuda.current_device() == d.index:
             hit[0].replay()
+        else:
+            with torch.cuda.device(d):
+                hit[0].replay()
         _GRAPH_NET += hit[3]
         return
     # capture on a side stream without torch.cuda.graph's synchronize /
