@@ -392,7 +392,9 @@ def test_float_map_many_moduli_and_near_midpoints(golden_streams):
 # lanes x blocks <= 2^23 take K1p (one thread per draw), larger ones K1s (segments)
 @pytest.mark.parametrize("mv,blocks,e", [(1, 1 << 18, 9), (1, 1 << 20, 3), (3, 40000, 5), (64, 20000, 65537),
                                          (100, 3000, 7), (2048, 100, 9), (1, 70, 17),
-                                         (64, (1 << 17) + 5, 9), (8, (1 << 20) + 3, 5), (1, (1 << 23) + 7, 3)])
+                                         (64, (1 << 17) + 5, 9), (8, (1 << 20) + 3, 5), (1, (1 << 23) + 7, 3),
+                                         # K1p at its largest segment indices (19- and 18-bit jump tables)
+                                         (1, 1 << 23, 9), (3, (1 << 21) + 1, 17)])
 def test_segmented_fill_equals_lane_fill(p0, mv, blocks, e):
     """rsa_fill_segmented (lanes split across threads: jump-ahead skip + scanned
     message sums) is bit-identical to the one-thread-per-lane rsa_fill, outputs
