@@ -12,6 +12,7 @@ state, so the scalar stream is the Mv = 1 case of the lane kernels.
 from __future__ import annotations
 
 import functools
+from collections import OrderedDict
 import math
 import weakref
 from dataclasses import dataclass
@@ -188,15 +189,38 @@ def _device_instance_cached(params: GeneratorParams, dev_index: int) -> torch.Te
     return torch.from_numpy(rec.view(np.uint8).copy()).to(torch.device("cuda", dev_index))
 
 
+# identity-keyed front caches: hashing a frozen GeneratorParams costs ~1 us
+# per lookup, a per-take cost on the launch path.  Each entry holds the params
+# object itself, so its id cannot be reused while the entry lives.
+_BY_ID: "OrderedDict[tuple, tuple]" = OrderedDict()
+_BY_ID_MAX = 256
+
+
+def _by_id(kind: str, params: GeneratorParams, idx, make):
+    key = (kind, id(params), idx)
+    hit = _BY_ID.get(key)
+    if hit is not None and hit[0] is params:
+        return hit[1]
+    val = make()
+    _BY_ID[key] = (params, val)
+    if len(_BY_ID) > _BY_ID_MAX:
+        _BY_ID.popitem(last=False)
+    return val
+
+
 def device_instance(params: GeneratorParams, dev=None) -> torch.Tensor:
     """128-byte rsa_instance on the device for one stream."""
     d = _device.device(dev)
-    return _device_instance_cached(params, d.index)
+    return _by_id("inst", params, d.index, lambda: _device_instance_cached(params, d.index))
 
 
 @functools.lru_cache(maxsize=256)
-def instance_flags(params: GeneratorParams) -> int:
+def _instance_flags(params: GeneratorParams) -> int:
     return int(_instance_record(params)[0]["flags"])
+
+
+def instance_flags(params: GeneratorParams) -> int:
+    return _by_id("flags", params, None, lambda: _instance_flags(params))
 
 
 def skip_only_instance(skip: SkipParams, dev=None) -> torch.Tensor:
