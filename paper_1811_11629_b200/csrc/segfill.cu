@@ -495,6 +495,7 @@ extern "C" uint64_t rsa_fill_segments(uint64_t lanes, uint64_t blocks) {
 #ifndef RSA_PD_MAX
 #define RSA_PD_MAX (1ull << 23)
 #endif
+static_assert(RSA_PD_MAX / PD_SEG <= (1ull << PD_TBITS), "k_pd_skips' jump table covers every segment index");
 static bool use_pd(uint64_t lanes, uint64_t blocks) {
     return blocks >= 4 * PD_SEG && lanes * blocks <= RSA_PD_MAX && rsa_fill_segments(lanes, blocks) > 1;
 }
