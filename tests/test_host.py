@@ -206,3 +206,39 @@ def test_fused_garner_bound():
                 h = r - p1 if r >= p1 else r
                 c1 = y1 * k1 * pow(R32, -1, p1) % p1
                 assert h == (c1 - c2) * p2inv % p1
+
+
+def test_identity_caches_follow_the_params_object(golden_regression):
+    """rsacore's per-take front caches are keyed by object identity and never
+    return another params object's entry."""
+    g = golden_regression["params"]
+    p = rsacore.make_params(g["p1"], g["p2"], g["e"], skipgen.SkipParams.create(g["a"]))
+    f1 = rsacore.instance_flags(p)
+    assert f1 == rsacore.instance_flags(p)
+    assert f1 == int(rsacore._instance_record(p)[0]["flags"])
+    # an equal-valued but distinct object gets its own (equal) entry
+    q = rsacore.make_params(g["p1"], g["p2"], g["e"], skipgen.SkipParams.create(g["a"]))
+    assert q is not p and rsacore.instance_flags(q) == f1
+
+
+def test_call_cache_follows_the_loaded_library(monkeypatch):
+    """_lib.call caches typed entry points per library object: replacing the
+    library (a reload) is honoured on the next call."""
+    from paper_1811_11629_b200 import _lib
+
+    class FakeLib:
+        def __init__(self, rc):
+            self.rc = rc
+            self.calls = 0
+
+        def rsa_fake(self, *a):
+            self.calls += 1
+            return self.rc
+
+    a, b = FakeLib(_lib.RSA_OK), FakeLib(_lib.RSA_OK)
+    monkeypatch.setattr(_lib, "_LIB", a)
+    _lib.call("rsa_fake", 1)
+    monkeypatch.setattr(_lib, "_LIB", b)
+    _lib.call("rsa_fake", 2)
+    assert (a.calls, b.calls) == (1, 1)
+    _lib._FN.pop("rsa_fake", None)
