@@ -326,7 +326,7 @@ k_pd_draws(const rsa_instance* __restrict__ inst, uint32_t mv, uint64_t blocks, 
     const uint32_t i = lane / mv;
     const uint32_t g = lane - i * mv;
     const FastInst P = load_fast(inst + i);
-    const int wl = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int wl = threadIdx.x & 31;
     const uint64_t d0 = (uint64_t)b * PD_CTA2 + (uint64_t)threadIdx.x * PD_DPT;  // this thread's first draw
     if (threadIdx.x < 32) {  // the lane's pass-1 CTA totals before this CTA's pass-1 CTA
         const uint32_t c1 = (uint32_t)(((uint64_t)b * PD_CTA2 / PD_SEG) / PD_BLOCK);
